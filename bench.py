@@ -1,0 +1,341 @@
+"""Benchmark: QPS at recall@10 >= 0.95, SIFT1M-shaped TSDG search, batch 10K (config C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one large-batch best-first search (paper Alg. 2) of the whole 10K-query
+batch over the 1M x 128 fp32 low-LID clustered set (SURVEY.md §8(d) recipe 2),
+TSDG built by the reference's CPU builder (nn_descent k=64 + build(1.2, 9),
+tools/make_dataset.py) and loaded unchanged.  Search parameters are fixed at the
+recall >= 0.95 operating point (k_search=16, delta=0, lambda_cut=5, m=8,
+T=1024, seed=7: recall@10 0.967 measured with the reference itself).
+
+ours:      `value` = device-resident throughput (queries already in HBM; CUDA events
+           on the launching stream around each step; L2 flushed between steps);
+           `e2e`   = same search through the reference-facing C-ABI call with HOST
+           buffers (pinned), H2D of the queries and D2H of ids/dists/counts inside
+           the timed region.
+reference: the reference's own CPU large_batch_search (oracle/_ref, unmodified,
+           OpenMP on all host cores) on the same config.
+Multi-GPU (torchrun, one process per GPU): the index is replicated; each rank
+searches its own 10K-query batch (query_index_base = rank * 10K, so every query
+keeps its reference RNG stream) — weak scaling, no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DATASET = "c2_lowlid_1m"
+PARAMS = dict(k=16, hop_limit=1024, delta=0.0, m_segments=8, lambda_cut=5, seed=7)
+METRIC = "QPS at recall@10>=0.95 (SIFT1M-shape 1Mx128 fp32 L2, batch 10K)"
+WORKLOAD = "C2: SIFT1M-shaped 1Mx128 fp32 L2 low-LID clustered, TSDG (reference nn_descent k=64 + build(1.2,9)), large batch 10K queries, best-first"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reference_arm(args, ds, ws, rank):
+    """The reference's own CPU implementation (oracle/_ref) on the same config."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2204_00824_b200.search import BestFirstParams
+
+    ref = O.Ref()
+    threads = ref.so.ref_num_threads()
+    fx = ref.fixture(ds.graph_path, ds.base)
+    p = BestFirstParams(**PARAMS)
+    nq_step = min(args.ref_queries, ds.queries.shape[0])
+    q = ds.queries[:nq_step]
+    for _ in range(args.warmup):
+        fx.large_batch(q, p)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ids, counts, st = fx.large_batch(q, p)
+    dt = time.perf_counter() - t0
+    qps = nq_step * args.steps / dt
+    rec = O.recall_at_k(ids, counts, ds.gt, 10)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (low-LID clustered, seeded)",
+        "config": {"workload": WORKLOAD, "params": PARAMS, "queries_per_step": nq_step,
+                   "recall_at_10": rec},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{nq_step} of the 10K C2 queries per step, reference "
+                                   f"large_batch_search (OpenMP, {threads} threads)"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(ds, seconds_budget=15.0):
+    """Reference CPU search on a bounded sample (rank 0, N=1)."""
+    from oracle import oracle as O
+    from paper_2204_00824_b200.search import BestFirstParams
+
+    ref = O.Ref()
+    threads = ref.so.ref_num_threads()
+    fx = ref.fixture(ds.graph_path, ds.base)
+    p = BestFirstParams(**PARAMS)
+    q = ds.queries[:500]
+    fx.large_batch(q, p)
+    t0 = time.perf_counter()
+    done = 0
+    while time.perf_counter() - t0 < seconds_budget and done < ds.queries.shape[0]:
+        chunk = ds.queries[done:done + 2000]
+        fx.large_batch(chunk, p)
+        done += chunk.shape[0]
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "queries/s", "cores": threads, "kind": "reference",
+            "sample": f"first {done} C2 queries, reference large_batch_search "
+                      f"(oracle/_ref, unmodified, OpenMP {threads} threads), ~{seconds_budget:.0f}s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-queries", type=int, default=10000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["det", "fast"], default="det")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+
+    from paper_2204_00824_b200 import datasets
+
+    if not datasets.available(DATASET):
+        raise SystemExit(f"data/{DATASET} missing: python tools/make_dataset.py --name {DATASET} "
+                         "--kind lowlid --n 1000000 --nq 10000 --d 128 --latent 16 "
+                         "--builder nndescent --knn-k 64 --iters 5")
+    ds = datasets.load(DATASET)
+
+    if args.impl == "reference":
+        reference_arm(args, ds, ws, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_00824_b200 import _native
+    from paper_2204_00824_b200.search import BestFirstParams, GpuIndex, load_tsdg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    graph = load_tsdg(ds.graph_path)
+    idx = GpuIndex(graph, ds.base, device=local)
+    p = BestFirstParams(**PARAMS)
+    mode = _native.MODE_DETERMINISTIC if args.mode == "det" else _native.MODE_FAST
+    nq, k = ds.queries.shape[0], p.k
+    qbase = rank * nq
+
+    stream = torch.cuda.Stream(device=dev)
+    sptr = stream.cuda_stream
+    dq = torch.from_numpy(ds.queries).to(dev)
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    d_counts = torch.empty(nq, dtype=torch.int32, device=dev)
+    d_stats = torch.empty((nq, 4), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        idx.search_bestfirst_device(dq.data_ptr(), nq, p, d_ids.data_ptr(), d_dists.data_ptr(),
+                                    d_counts.data_ptr(), d_stats.data_ptr(), sptr,
+                                    query_index_base=qbase, mode=mode)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    ids = d_ids.cpu().numpy().view(np.uint32)
+    counts = d_counts.cpu().numpy().view(np.uint32)
+    stats = d_stats.cpu().numpy().astype(np.uint64)
+    from oracle.oracle import recall_at_k  # checker only: recall of the timed configuration
+    rec = recall_at_k(ids, counts, ds.gt, 10)
+    d = ds.base.shape[1]
+    evals, examined = stats[:, 1].sum(), stats[:, 3].sum()
+    alg_bytes = int(4 * d * evals + 4 * examined + nq * (4 * d + 8 * k))
+
+    # ---- device-resident timed region --------------------------------------------
+    launches0 = _native.lib().tsdg_gpu_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(float(i))  # L2 flush outside the events
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = _native.lib().tsdg_gpu_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = sum(step_ms) / 1e3
+    if ws > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+        dist.barrier()
+    value = nq * ws * args.steps / total_s
+    kernel_s = total_s / args.steps  # one search kernel per step (+ a 4-byte counter memset)
+
+    # ---- end-to-end through the host-pointer C-ABI call -----------------------------
+    hq = torch.from_numpy(ds.queries).pin_memory()
+    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    h_c = torch.empty(nq, dtype=torch.int32).pin_memory()
+    pc = p.c()
+    L = _native.lib()
+
+    def e2e_step():
+        _native.check(L.tsdg_gpu_search_bestfirst(
+            idx.handle, ctypes.c_void_p(hq.data_ptr()), nq, qbase, ctypes.byref(pc), mode,
+            ctypes.c_void_p(h_ids.data_ptr()), ctypes.c_void_p(h_d.data_ptr()),
+            ctypes.c_void_p(h_c.data_ptr()), None))
+
+    for _ in range(2):
+        e2e_step()
+    if ws > 1:
+        dist.barrier()
+    e2e_times = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()  # synchronous: returns after the D2H copies landed
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times)
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = nq * ws * args.steps / e2e_s
+    assert np.array_equal(h_ids.numpy().view(np.uint32), ids), "e2e result differs"
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        achieved = alg_bytes / kernel_s / 1e9
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(ds)
+            except Exception as e:  # reference not built on this host
+                cpu = {"value": None, "unavailable": str(e)}
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (low-LID clustered generator, seeded); graph built by the reference CPU builder",
+            "config": {"workload": WORKLOAD, "params": PARAMS, "mode": args.mode,
+                       "queries_per_gpu": nq, "global_batch": nq * ws,
+                       "parallelism": f"replicated index, query split x{ws}",
+                       "recall_at_10": rec, "l2": "flushed between timed steps (256 MB write); "
+                       "inputs also exceed L2 (512 MB vectors + padded adjacency)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "alg_bytes_per_step": alg_bytes,
+                         "alg_bytes_formula": "4*d*E_q + 4*A_q + 4*d + 8*k summed over queries",
+                         "evals_per_query": float(evals) / nq,
+                         "edges_per_query": float(examined) / nq},
+            "e2e": {"value": e2e_val, "unit": "queries/s",
+                    "h2d_bytes_per_step": int(ds.queries.nbytes),
+                    "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * tsdg_gpu.h — C-ABI of the B200 (sm_100a) TSDG search library
+ * (paper_2204_00824_b200/_lib/libtsdg_gpu.so).
+ *
+ * Drop-in boundary for the reference's search hot path.  The reference is a
+ * C++20 library (/root/reference/proj); its search entry points run an OpenMP
+ * loop over queries, and this ABI sits exactly where that loop sits
+ * (SURVEY.md §3).  Each entry point below names the reference interface it
+ * replaces.  Plain pointers and sizes only; no STL, no torch types.
+ *
+ * Error convention: every call returns TSDG_OK (0) or a status code; the
+ * message is in tsdg_gpu_last_error() (thread-local).  The C++ wrapper
+ * (include/tsdg/gpu_search.hpp) rethrows TSDG_EINVAL as std::invalid_argument
+ * and TSDG_ERUNTIME as std::runtime_error, the exception types the reference
+ * throws (bestfirst_search.cpp:116-120,134; greedy_search.cpp:30-35,78-82,112;
+ * diversify.cpp:254,276,281-282).
+ *
+ * Determinism: TSDG_MODE_DETERMINISTIC reproduces the reference bit for bit
+ * (ids, fp32 distances, hops / distance_evals / queue_evictions per query).
+ * TSDG_MODE_FAST is allowed to differ in fp32 rounding of distances only
+ * (fused multiply-add, tree reduction); its recall must stay within 0.5 points
+ * of the reference at equal parameters.
+ */
+#ifndef TSDG_GPU_H
+#define TSDG_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSDG_GPU_ABI_VERSION 1
+
+enum {
+    TSDG_OK = 0,
+    TSDG_EINVAL = 1,   /* std::invalid_argument in the reference */
+    TSDG_ERUNTIME = 2, /* std::runtime_error / CUDA failure */
+    TSDG_ENCCL = 3
+};
+
+enum { TSDG_MODE_DETERMINISTIC = 0, TSDG_MODE_FAST = 1 };
+
+enum { TSDG_METRIC_L2 = 0, TSDG_METRIC_COSINE = 1, TSDG_METRIC_IP = 2 }; /* vectors.hpp:15 */
+
+/* tsdg::BestFirstParams (bestfirst_search.hpp:15-25); same fields, same defaults
+ * (k=10, hop_limit=1024, delta=0, m_segments=8, lambda_cut=5, seed=0, unbounded=0). */
+typedef struct {
+    uint32_t k;
+    uint32_t hop_limit;
+    float delta;
+    uint32_t m_segments;
+    uint32_t lambda_cut;
+    uint64_t seed;
+    int32_t unbounded;
+} tsdg_bf_params;
+
+/* tsdg::GreedyParams (greedy_search.hpp:14-19); defaults t0=16, hop_limit=16,
+ * lambda_cut=10, seed=0. */
+typedef struct {
+    uint32_t t0;
+    uint32_t hop_limit;
+    uint32_t lambda_cut;
+    uint64_t seed;
+} tsdg_greedy_params;
+
+/* Per-query counters; tsdg::SearchStats (greedy_search.hpp:21-32) fields plus
+ * the EdgeTrace sizes (bestfirst_search.hpp:29-32). */
+typedef struct {
+    uint32_t hops;
+    uint32_t distance_evals;
+    uint32_t queue_evictions;
+    uint32_t edges_examined; /* EdgeTrace::examined.size() (greedy: streamed edges) */
+} tsdg_query_stats;
+
+/* TSDG file header (diversify.cpp:252-272). */
+typedef struct {
+    uint64_t n;
+    uint64_t num_edges;
+    uint32_t k;
+    float alpha;
+    uint16_t lambda0;
+    uint8_t metric;
+    uint32_t max_degree;
+} tsdg_graph_header;
+
+typedef struct tsdg_gpu_index tsdg_gpu_index;
+
+const char* tsdg_gpu_last_error(void);
+int tsdg_gpu_abi_version(void);
+
+/* ---- bulk TSDG loader (replaces load_tsdg, diversify.cpp:274-306) ----------
+ * Reads the reference's byte format unchanged: one sequential pass, no per-field
+ * stream calls.  tsdg_read_tsdg fills caller arrays sized from the header
+ * (offsets n+1, the rest num_edges); any pointer may be NULL to skip. */
+int tsdg_read_tsdg_header(const char* path, tsdg_graph_header* out);
+int tsdg_read_tsdg(const char* path, uint64_t* offsets, uint32_t* targets,
+                   uint16_t* lambdas, float* dists);
+
+/* ---- device index -----------------------------------------------------------
+ * Uploads the fp32 vector store (rows padded to 16 B) and a fixed-degree padded
+ * adjacency (row stride = max degree rounded up to 4, CSR order kept exactly,
+ * pads 0xFFFFFFFF) plus the per-edge lambda for deg_cut.  Replaces the
+ * reference's in-RAM TsdgGraph + VectorSet (diversify.hpp:56-76, vectors.hpp:23-34). */
+int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint64_t* offsets,
+                          const uint32_t* targets, const uint16_t* lambdas, int metric,
+                          int device, tsdg_gpu_index** out);
+int tsdg_gpu_index_create_from_file(const char* tsdg_path, const float* base, uint32_t n,
+                                    uint32_t d, int device, tsdg_gpu_index** out);
+int tsdg_gpu_index_destroy(tsdg_gpu_index* idx);
+/* n, d, metric, max_degree, device, padded row stride (floats), adjacency stride */
+int tsdg_gpu_index_info(const tsdg_gpu_index* idx, uint32_t* n, uint32_t* d, int* metric,
+                        uint32_t* max_degree, int* device, uint32_t* row_stride,
+                        uint32_t* adj_stride);
+/* deg_cut: per-node lambda-prefix length for a cutoff (diversify.cpp:34-42), kept
+ * cached in the index; copies it out when out != NULL (n entries). */
+int tsdg_gpu_deg_cut(tsdg_gpu_index* idx, uint32_t lambda_cut, uint32_t* out);
+
+/* ---- large batch: best-first, Alg. 2 ------------------------------------------
+ * Replaces tsdg::large_batch_search (bestfirst_search.cpp:129-150).  Query q uses
+ * the stream Rng64(params.seed).fork(query_index_base + q); with base 0 this is the
+ * reference batch call, and a split batch (multi-GPU) passes its slice start.
+ * ids: nq x k, ascending by (dist, id), padded 0xFFFFFFFF; dists padded +inf;
+ * counts: nq; stats: nq entries or NULL.  HOST pointers; all copies inside. */
+int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                              uint64_t query_index_base, const tsdg_bf_params* params,
+                              int mode, uint32_t* ids, float* dists, uint32_t* counts,
+                              tsdg_query_stats* stats);
+/* Same, DEVICE pointers, asynchronous on `stream` (cudaStream_t; NULL = legacy). */
+int tsdg_gpu_search_bestfirst_device(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
+                                     uint64_t query_index_base, const tsdg_bf_params* params,
+                                     int mode, uint32_t* d_ids, float* d_dists,
+                                     uint32_t* d_counts, tsdg_query_stats* d_stats,
+                                     void* stream);
+
+/* ---- small batch: multi-start greedy, Alg. 1 --------------------------------
+ * Replaces tsdg::small_batch_search (greedy_search.cpp:106-127): t0 walks per query
+ * with streams Rng64(seed).fork(s) (the same for every query), merged by
+ * (dist, id) with id-dedup, first k.  Output layout as for best-first. */
+int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t nq, uint32_t k,
+                           const tsdg_greedy_params* params, int mode, uint32_t* ids,
+                           float* dists, uint32_t* counts, tsdg_query_stats* stats);
+int tsdg_gpu_search_greedy_device(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
+                                  uint32_t k, const tsdg_greedy_params* params, int mode,
+                                  uint32_t* d_ids, float* d_dists, uint32_t* d_counts,
+                                  tsdg_query_stats* d_stats, void* stream);
+/* One greedy walk (greedy_search.cpp:27-72) per query with an explicit RNG state
+ * per query (rng_states[q]): the 32-slot R_ij is written to ids32/dists32 (nq x 32). */
+int tsdg_gpu_greedy_once(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                         const uint64_t* rng_states, uint32_t hop_limit, uint32_t lambda_cut,
+                         uint32_t* ids32, float* dists32, tsdg_query_stats* stats);
+
+/* ---- sharded base: per-shard top-k merge (no reference counterpart) ----------
+ * After an all-gather of S shards' results (each nq x k, LOCAL ids, ascending),
+ * merges per query by (dist, global id), global id = shard_base[s] + local id.
+ * DEVICE pointers; layout [s][q][k]. */
+int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
+                                 const uint32_t* d_counts, const uint64_t* shard_base,
+                                 uint32_t shards, uint32_t nq, uint32_t k, uint32_t* d_out_ids,
+                                 float* d_out_dists, uint32_t* d_out_counts, void* stream);
+
+/* Number of kernels this library launched since load (evidence counter). */
+uint64_t tsdg_gpu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSDG_GPU_H */

@@ -1,0 +1,65 @@
+"""In-tree build of every native artefact (called by __graft_entry__.build()).
+
+  _lib/libtsdg_gpu.so      CUDA kernels + C-ABI (nvcc, sm_100a only)
+  _lib/libtsdg_datagen.so  synthetic input generators (gcc)
+  oracle/libtsdg_oracle.so CPU oracle restatement (test infrastructure)
+  oracle/_ref/*            the reference compiled from /root/reference when present
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "_lib")
+CSRC = os.path.join(HERE, "csrc")
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd, cwd=ROOT):
+    print("[build]", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def _stale(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_gpu(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "libtsdg_gpu.so")
+    srcs = [os.path.join(CSRC, f) for f in ("tsdg_gpu.cu", "tsdg_io.cpp")]
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    deps.append(os.path.join(ROOT, "include", "tsdg_gpu.h"))
+    if force or _stale(out, deps):
+        _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+              "-shared", "-o", out, *srcs])
+    return out
+
+
+def build_datagen(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "libtsdg_datagen.so")
+    src = os.path.join(ROOT, "tools", "datagen.c")
+    if force or _stale(out, [src]):
+        _run(["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+              "-o", out, src, "-lm"])
+    return out
+
+
+def build_oracle() -> None:
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"])
+    if os.path.isdir("/root/reference/proj/src"):
+        _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle"), "ref"])
+
+
+def build_all(force: bool = False) -> None:
+    build_datagen(force)
+    build_oracle()
+    build_gpu(force)

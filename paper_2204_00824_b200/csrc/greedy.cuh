@@ -1,0 +1,386 @@
+// Small-batch multi-start greedy search (paper Alg. 1), deterministic.
+//
+// greedy_walk_kernel: one warp per (query, walk s).  Restates greedy_search_once
+// (greedy_search.cpp:27-72) with select_start (:12-25):
+//   - 32 start draws from stream Rng64(seed).fork(s) (the same streams for every
+//     query of a call, greedy_search.cpp:83,88) — or an explicit state per walk;
+//   - per hop, the lambda-prefix of u streams through the 32 lanes in groups of 32
+//     (lane = position mod 32): lane j keeps its own R_temp slot with the strict-<
+//     per-lane minimum of lane_update (rank_list.cpp:8-18) in registers;
+//   - merge_halves (rank_list.cpp:20-49) as a warp operation: bitonic sort of
+//     R_temp, id-dedup of its best 16 finite entries against R_ij by shuffles,
+//     then a 64-key bitonic sort of (R_ij, newcomers) keeping the first 32;
+//   - u <- closest of R_temp (not R_ij); stop when the merge changed nothing.
+// Rows are staged with the same TMA bulk-copy gather as the best-first kernel,
+// so distances are the reference's sequential fp32 values bit for bit.
+//
+// greedy_merge_kernel: one CTA per query merges the t0 walks' 32-slot lists:
+// finite entries, sort by (dist, id), unique by id, first k
+// (greedy_search.cpp:85-103).
+#pragma once
+
+#include "bestfirst.cuh"
+
+namespace tsdg_dev {
+
+constexpr int kGrWarps = 4;
+
+struct GrArgs {
+    const float* vec;
+    const uint32_t* adj;
+    const uint32_t* degcut;
+    const float* queries;
+    uint32_t ld, R, n, d;
+    uint32_t nq, t0, hop_limit;
+    uint64_t seed;
+    const uint64_t* walk_states;  // optional: explicit RNG state per walk
+    uint32_t* walk_ids;           // (nq*t0) x 32
+    float* walk_dists;
+    uint32_t* walk_hops;          // nq*t0
+    uint32_t* walk_evals;
+    uint32_t* work_counter;
+    uint32_t dch;
+    uint32_t warp_smem, off_query, off_stage, off_bar;
+};
+
+// compare-exchange keeping min (keep_min) or max of (d,id) vs partner's
+__device__ __forceinline__ void cx(float& d, uint32_t& id, float od, uint32_t oi, bool keep_min) {
+    const bool other_first = closer(od, oi, d, id);
+    if (keep_min == other_first) {
+        d = od;
+        id = oi;
+    }
+}
+
+// Ascending bitonic sort of 32 keys, one per lane.
+__device__ __forceinline__ void warp_sort32(float& d, uint32_t& id, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const float od = __shfl_xor_sync(kFull, d, j);
+            const uint32_t oi = __shfl_xor_sync(kFull, id, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            cx(d, id, od, oi, lower == up);
+        }
+    }
+}
+
+// Ascending bitonic sort of 64 keys: (da,ia) is index lane, (db,ib) index 32+lane.
+__device__ __forceinline__ void warp_sort64(float& da, uint32_t& ia, float& db, uint32_t& ib,
+                                            int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // only at k == 64: ascending, a keeps min
+                const bool b_first = closer(db, ib, da, ia);
+                if (b_first) {
+                    const float td = da;
+                    const uint32_t ti = ia;
+                    da = db;
+                    ia = ib;
+                    db = td;
+                    ib = ti;
+                }
+            } else {
+                const float oda = __shfl_xor_sync(kFull, da, j);
+                const uint32_t oia = __shfl_xor_sync(kFull, ia, j);
+                const float odb = __shfl_xor_sync(kFull, db, j);
+                const uint32_t oib = __shfl_xor_sync(kFull, ib, j);
+                const bool lower = (lane & j) == 0;
+                const bool up_a = (lane & k) == 0;
+                const bool up_b = ((lane + 32) & k) == 0;
+                cx(da, ia, oda, oia, lower == up_a);
+                cx(db, ib, odb, oib, lower == up_b);
+            }
+        }
+    }
+}
+
+// merge_halves (rank_list.cpp:20-49).  (rd, ri): R_ij slot `lane` (sorted);
+// (td, ti): R_temp slot `lane`.  Returns the warp-uniform "updated".
+__device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float td,
+                                                  uint32_t ti, int lane) {
+    const float kInf = __int_as_float(0x7f800000);
+    warp_sort32(td, ti, lane);  // incoming, ascending
+    const bool cand = lane < 16 && ti != kInvalid;
+    int found = -1;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+        const uint32_t oi = __shfl_sync(kFull, ri, t);
+        if (cand && found < 0 && oi == ti) found = t;
+    }
+    // in-place replacement when the newcomer is closer than its duplicate
+    float nd = rd;
+    uint32_t ni = ri;
+#pragma unroll 4
+    for (int src = 0; src < 16; ++src) {
+        const int f = __shfl_sync(kFull, found, src);
+        const float sd = __shfl_sync(kFull, td, src);
+        const uint32_t sid = __shfl_sync(kFull, ti, src);
+        if (f == lane && closer(sd, sid, nd, ni)) {
+            nd = sd;
+            ni = sid;
+        }
+    }
+    float bd = (cand && found < 0) ? td : kInf;
+    uint32_t bi = (cand && found < 0) ? ti : kInvalid;
+    warp_sort64(nd, ni, bd, bi, lane);
+    const bool changed = (nd != rd) || (ni != ri);
+    rd = nd;
+    ri = ni;
+    return __any_sync(kFull, changed);
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    unsigned char* ws = smem_raw + (threadIdx.x >> 5) * a.warp_smem;
+    BfWarp w;  // only sq / stage / bar / parity are used
+    w.sq = reinterpret_cast<float*>(ws + a.off_query);
+    w.stage = reinterpret_cast<float*>(ws + a.off_stage);
+    w.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
+    w.parity = 0;
+    BfArgs g{};  // geometry view for gather_distances
+    g.vec = a.vec;
+    g.ld = a.ld;
+    g.d = a.d;
+    g.dch = a.dch;
+    if (lane == 0) mbar_init(w.bar, 1);
+    __syncwarp();
+    const float kInf = __int_as_float(0x7f800000);
+    const uint32_t nwalks = a.nq * a.t0;
+    uint32_t cur_q = kInvalid;
+
+    for (;;) {
+        uint32_t wk = 0;
+        if (lane == 0) wk = atomicAdd(a.work_counter, 1u);
+        wk = __shfl_sync(kFull, wk, 0);
+        if (wk >= nwalks) break;
+        const uint32_t q = wk / a.t0;
+        const uint32_t s = wk % a.t0;
+        if (q != cur_q) {
+            __syncwarp();
+            const float* gq = a.queries + (size_t)q * a.d;
+            for (uint32_t i = lane; i < a.ld; i += 32) w.sq[i] = i < a.d ? gq[i] : 0.0f;
+            cur_q = q;
+            __syncwarp();
+        }
+        const uint64_t st = a.walk_states ? a.walk_states[wk] : fork_state(a.seed, s);
+
+        // select_start (greedy_search.cpp:12-25)
+        const uint32_t v = draw_below(st, (uint32_t)lane, a.n);
+        float sd = gather_distances<METRIC>(w, g, true, v, lane);
+        uint32_t si = v;
+        warp_argmin(sd, si);
+        uint32_t u = si;
+        uint32_t evals = 32, t = 0;
+
+        float rd = kInf;
+        uint32_t ri = kInvalid;
+        bool improved = true;
+        while (improved && t < a.hop_limit) {
+            ++t;
+            float td = kInf;
+            uint32_t ti = kInvalid;
+            const uint32_t deg = __ldg(a.degcut + u);
+            const uint32_t* arow = a.adj + (size_t)u * a.R;
+            for (uint32_t base = 0; base < deg; base += 32) {
+                const uint32_t j = base + lane;
+                const bool valid = j < deg;
+                const uint32_t e = valid ? __ldg(arow + j) : kInvalid;
+                const float dist = gather_distances<METRIC>(w, g, valid, e, lane);
+                if (valid && dist < td) {  // lane_update: strict <, earlier group keeps ties
+                    td = dist;
+                    ti = e;
+                }
+            }
+            evals += deg;
+            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
+            float nd = td;
+            uint32_t ni = ti;
+            warp_argmin(nd, ni);
+            if (ni != kInvalid) u = ni;
+            improved = updated;
+        }
+        a.walk_ids[(size_t)wk * 32 + lane] = ri;
+        a.walk_dists[(size_t)wk * 32 + lane] = rd;
+        if (lane == 0) {
+            a.walk_hops[wk] = t;
+            a.walk_evals[wk] = evals;
+        }
+    }
+}
+
+// One CTA per query: pool the t0 x 32 walk slots, sort, unique, first k.
+constexpr int kMergeThreads = 256;
+
+__global__ void __launch_bounds__(kMergeThreads) greedy_merge_kernel(
+    const uint32_t* walk_ids, const float* walk_dists, const uint32_t* walk_hops,
+    const uint32_t* walk_evals, uint32_t t0, uint32_t k, uint32_t npow2, uint32_t* out_ids,
+    float* out_dists, uint32_t* out_counts, tsdg_query_stats* out_stats) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* sd = reinterpret_cast<float*>(smem_raw);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sd + npow2);
+    uint32_t* scan = si + npow2;  // kMergeThreads + 1
+    const uint32_t q = blockIdx.x;
+    const uint32_t total = t0 * 32;
+    const float kInf = __int_as_float(0x7f800000);
+    for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+        float d = kInf;
+        uint32_t id = kInvalid;
+        if (i < total) {
+            id = walk_ids[(size_t)q * total + i];
+            d = id != kInvalid ? walk_dists[(size_t)q * total + i] : kInf;
+        }
+        sd[i] = d;
+        si[i] = id;
+    }
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= npow2; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+                const uint32_t p = i ^ j;
+                if (p > i) {
+                    const bool up = (i & kk) == 0;
+                    const bool p_first = closer(sd[p], si[p], sd[i], si[i]);
+                    if (p_first == up) {
+                        const float td = sd[i];
+                        const uint32_t ti = si[i];
+                        sd[i] = sd[p];
+                        si[i] = si[p];
+                        sd[p] = td;
+                        si[p] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // unique by id over adjacent entries (std::unique), then first k
+    const uint32_t per = (npow2 + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t cnt = 0;
+    for (uint32_t i = b0; i < b0 + per && i < npow2; ++i)
+        cnt += (si[i] != kInvalid && (i == 0 || si[i] != si[i - 1])) ? 1u : 0u;
+    scan[threadIdx.x] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t t = 0; t < blockDim.x; ++t) {
+            const uint32_t c = scan[t];
+            scan[t] = run;
+            run += c;
+        }
+        scan[blockDim.x] = run;
+    }
+    __syncthreads();
+    uint32_t pos = scan[threadIdx.x];
+    for (uint32_t i = b0; i < b0 + per && i < npow2; ++i) {
+        if (si[i] != kInvalid && (i == 0 || si[i] != si[i - 1])) {
+            if (pos < k) {
+                out_ids[(size_t)q * k + pos] = si[i];
+                if (out_dists) out_dists[(size_t)q * k + pos] = sd[i];
+            }
+            ++pos;
+        }
+    }
+    const uint32_t uniq = scan[blockDim.x];
+    const uint32_t c = uniq < k ? uniq : k;
+    for (uint32_t i = c + threadIdx.x; i < k; i += blockDim.x) {
+        out_ids[(size_t)q * k + i] = kInvalid;
+        if (out_dists) out_dists[(size_t)q * k + i] = kInf;
+    }
+    if (threadIdx.x == 0) {
+        if (out_counts) out_counts[q] = c;
+        if (out_stats) {
+            uint32_t h = 0, e = 0;
+            for (uint32_t s = 0; s < t0; ++s) {
+                h += walk_hops[(size_t)q * t0 + s];
+                e += walk_evals[(size_t)q * t0 + s];
+            }
+            tsdg_query_stats st;
+            st.hops = h;
+            st.distance_evals = e;
+            st.queue_evictions = 0;
+            st.edges_examined = e - 32u * t0;
+            out_stats[q] = st;
+        }
+    }
+}
+
+// deg_cut: partition_point(lambda < cut) over each node's edges (diversify.cpp:34-42).
+__global__ void deg_cut_kernel(const uint16_t* lam, uint32_t R, const uint32_t* deg_full,
+                               uint32_t n, uint32_t cut, uint32_t* out) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const uint16_t* row = lam + (size_t)u * R;
+    uint32_t lo = 0, hi = deg_full[u];
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint32_t)row[mid] < cut) lo = mid + 1;
+        else hi = mid;
+    }
+    out[u] = lo;
+}
+
+// Sharded-base merge: per query, union of S shard lists (local ids + base),
+// ascending by (dist, global id), first k.  One CTA per query, smem bitonic.
+__global__ void __launch_bounds__(kMergeThreads) merge_shards_kernel(
+    const uint32_t* ids, const float* dists, const uint32_t* counts, const uint64_t* shard_base,
+    uint32_t S, uint32_t nq, uint32_t k, uint32_t npow2, uint32_t* out_ids, float* out_dists,
+    uint32_t* out_counts) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* sd = reinterpret_cast<float*>(smem_raw);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sd + npow2);
+    const uint32_t q = blockIdx.x;
+    const float kInf = __int_as_float(0x7f800000);
+    uint32_t valid_total = 0;
+    for (uint32_t s = 0; s < S; ++s) valid_total += min(counts[(size_t)s * nq + q], k);
+    for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+        float d = kInf;
+        uint32_t id = kInvalid;
+        if (i < S * k) {
+            const uint32_t s = i / k, j = i % k;
+            if (j < counts[(size_t)s * nq + q]) {
+                const size_t off = ((size_t)s * nq + q) * k + j;
+                id = (uint32_t)(shard_base[s] + ids[off]);
+                d = dists[off];
+            }
+        }
+        sd[i] = d;
+        si[i] = id;
+    }
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= npow2; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+                const uint32_t p = i ^ j;
+                if (p > i) {
+                    const bool up = (i & kk) == 0;
+                    const bool p_first = closer(sd[p], si[p], sd[i], si[i]);
+                    if (p_first == up) {
+                        const float td = sd[i];
+                        const uint32_t ti = si[i];
+                        sd[i] = sd[p];
+                        si[i] = si[p];
+                        sd[p] = td;
+                        si[p] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const uint32_t c = valid_total < k ? valid_total : k;
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        out_ids[(size_t)q * k + i] = i < c ? si[i] : kInvalid;
+        out_dists[(size_t)q * k + i] = i < c ? sd[i] : kInf;
+    }
+    if (threadIdx.x == 0 && out_counts) out_counts[q] = c;
+}
+
+}  // namespace tsdg_dev

@@ -1,0 +1,651 @@
+// Host side of libtsdg_gpu.so: the C-ABI declared in include/tsdg_gpu.h.
+//
+// Owns the device index (vector store + padded adjacency + lambdas + cached
+// deg_cut tables), validates parameters exactly like the reference front ends
+// (bestfirst_search.cpp:112-150, greedy_search.cpp:74-127), sizes the
+// persistent kernels for occupancy on the B200's 148 SMs and launches them.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tsdg_gpu.h"
+#include "greedy.cuh"
+
+using namespace tsdg_dev;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(TSDG_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TSDG_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TSDG_ERUNTIME;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+uint32_t round_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+void tsdg_set_error(const std::string& msg) { g_err = msg; }
+
+struct tsdg_gpu_index {
+    int device = 0;
+    int sm_count = 148;
+    uint32_t n = 0, d = 0, ld = 0, R = 0, max_degree = 0;
+    int metric = 0;
+    float* vec = nullptr;
+    uint32_t* adj = nullptr;
+    uint16_t* lam = nullptr;
+    uint32_t* deg_full = nullptr;
+    uint32_t* counters = nullptr;  // work counters, one per launch slot
+    uint32_t counter_slot = 0;
+    std::map<uint32_t, uint32_t*> degcut;
+    std::mutex mu;
+    cudaStream_t stream = nullptr;  // for the host-pointer entry points
+};
+
+namespace {
+
+constexpr uint32_t kCounterSlots = 64;
+
+uint32_t* next_counter(tsdg_gpu_index* idx, cudaStream_t st) {
+    uint32_t* c = idx->counters + (idx->counter_slot++ % kCounterSlots);
+    cuda_check(cudaMemsetAsync(c, 0, sizeof(uint32_t), st), "cudaMemsetAsync(counter)");
+    return c;
+}
+
+const uint32_t* get_degcut(tsdg_gpu_index* idx, uint32_t cut, cudaStream_t st) {
+    auto it = idx->degcut.find(cut);
+    if (it != idx->degcut.end()) return it->second;
+    uint32_t* out = nullptr;
+    cuda_check(cudaMalloc(&out, sizeof(uint32_t) * std::max<uint32_t>(idx->n, 1)), "cudaMalloc(degcut)");
+    if (idx->n) {
+        deg_cut_kernel<<<(idx->n + 255) / 256, 256, 0, st>>>(idx->lam, idx->R, idx->deg_full,
+                                                             idx->n, cut, out);
+        g_launches++;
+        cuda_check(cudaGetLastError(), "deg_cut_kernel");
+    }
+    idx->degcut[cut] = out;
+    return out;
+}
+
+// Staged dims per row per gather round: the whole (padded) row when it fits in
+// 128 floats, else 128-float chunks.
+uint32_t staging_dims(uint32_t ld) { return std::min<uint32_t>(round_up(ld, 8), 128); }
+
+struct Carve {
+    uint32_t total = 0;
+    uint32_t take(uint32_t bytes, uint32_t align = 16) {
+        total = round_up(total, align);
+        const uint32_t off = total;
+        total += bytes;
+        return off;
+    }
+};
+
+void fill_bf_layout(BfArgs& a) {
+    Carve c;
+    a.off_bar = c.take(8, 8);
+    a.off_query = c.take(a.ld * 4);
+    a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
+    a.off_cid = c.take(a.P * 32 * 4);
+    a.off_cdist = c.take(a.P * 32 * 4);
+    a.off_csize = c.take(a.m * 4);
+    a.off_vid = c.take(a.P * 32 * 4);
+    a.off_vsize = c.take(a.m * 4);
+    a.off_voldest = c.take(a.m * 4);
+    a.off_rid = c.take(round_up(a.k + 2, 32) * 4);
+    a.off_rdist = c.take(round_up(a.k + 2, 32) * 4);
+    a.warp_smem = round_up(c.total, 128);
+}
+
+template <class K>
+int grid_for(K kernel, int threads, size_t smem, int sm_count, uint32_t work_warps,
+             int warps_per_cta) {
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) fail(TSDG_ERUNTIME, "kernel does not fit on an SM (shared memory)");
+    const uint32_t need = (work_warps + warps_per_cta - 1) / warps_per_cta;
+    return (int)std::max<uint32_t>(1, std::min<uint32_t>(need, (uint32_t)(per_sm * sm_count)));
+}
+
+void validate_bf(const tsdg_gpu_index* idx, const tsdg_bf_params* p) {
+    if (!p) fail(TSDG_EINVAL, "bestfirst_search: null params");
+    if (idx->n == 0) fail(TSDG_EINVAL, "bestfirst_search: empty graph");
+    if (p->k < 1 || p->hop_limit < 1 || p->m_segments < 1 || p->lambda_cut < 1 ||
+        p->delta < 0.0f || std::isnan(p->delta))
+        fail(TSDG_EINVAL, "bestfirst_search: invalid parameters");
+    if (p->unbounded)
+        fail(TSDG_EINVAL, "bestfirst_search: unbounded=true (exact std::set queue) is not "
+                          "implemented on the GPU path");
+    if (p->m_segments > 32) fail(TSDG_EINVAL, "bestfirst_search: GPU path supports m_segments <= 32");
+    if (p->k > 1024) fail(TSDG_EINVAL, "bestfirst_search: GPU path supports k <= 1024");
+}
+
+void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint64_t qbase,
+                      const tsdg_bf_params* p, int mode, uint32_t* d_ids, float* d_dists,
+                      uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
+    (void)mode;
+    if (nq == 0) return;
+    BfArgs a{};
+    a.vec = idx->vec;
+    a.adj = idx->adj;
+    a.degcut = get_degcut(idx, p->lambda_cut, st);
+    a.queries = d_queries;
+    a.ld = idx->ld;
+    a.R = idx->R;
+    a.n = idx->n;
+    a.d = idx->d;
+    a.nq = nq;
+    a.qbase = qbase;
+    a.k = p->k;
+    a.hop_limit = p->hop_limit;
+    a.delta = p->delta;
+    a.m = p->m_segments;
+    a.P = (a.m & 1u) ? a.m : a.m + 1;
+    a.seed = p->seed;
+    a.out_ids = d_ids;
+    a.out_dists = d_dists;
+    a.out_counts = d_counts;
+    a.out_stats = d_stats;
+    a.work_counter = next_counter(idx, st);
+    a.dch = staging_dims(idx->ld);
+    fill_bf_layout(a);
+    const size_t smem = (size_t)a.warp_smem * kBfWarps;
+    void (*kern)(BfArgs) = idx->metric == 0   ? bf_det_kernel<0>
+                           : idx->metric == 1 ? bf_det_kernel<1>
+                                              : bf_det_kernel<2>;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute(bf)");
+    const int grid = grid_for(kern, kBfWarps * 32, smem, idx->sm_count, nq, kBfWarps);
+    kern<<<grid, kBfWarps * 32, smem, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "bf_det_kernel launch");
+}
+
+void validate_greedy(const tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* p) {
+    if (!p) fail(TSDG_EINVAL, "small_batch_search: null params");
+    if (k < 1) fail(TSDG_EINVAL, "small_batch_search: k must be >= 1");
+    if (p->t0 < 1) fail(TSDG_EINVAL, "small_batch_search: t0 must be >= 1");
+    if ((uint64_t)k > 32ull * p->t0) fail(TSDG_EINVAL, "small_batch_search: k exceeds 32 * t0");
+    if (p->lambda_cut < 1) fail(TSDG_EINVAL, "greedy_search_once: lambda_cut must be >= 1");
+    if (p->hop_limit < 1) fail(TSDG_EINVAL, "greedy_search_once: hop limit must be >= 1");
+    if (idx->n == 0) fail(TSDG_EINVAL, "select_start: empty graph");
+    if (p->t0 > 256) fail(TSDG_EINVAL, "small_batch_search: GPU path supports t0 <= 256");
+}
+
+struct WalkBuffers {
+    uint32_t* ids = nullptr;
+    float* dists = nullptr;
+    uint32_t* hops = nullptr;
+    uint32_t* evals = nullptr;
+};
+
+WalkBuffers alloc_walks(uint32_t walks, cudaStream_t st) {
+    WalkBuffers b;
+    cuda_check(cudaMallocAsync(&b.ids, sizeof(uint32_t) * 32 * walks, st), "cudaMallocAsync");
+    cuda_check(cudaMallocAsync(&b.dists, sizeof(float) * 32 * walks, st), "cudaMallocAsync");
+    cuda_check(cudaMallocAsync(&b.hops, sizeof(uint32_t) * walks, st), "cudaMallocAsync");
+    cuda_check(cudaMallocAsync(&b.evals, sizeof(uint32_t) * walks, st), "cudaMallocAsync");
+    return b;
+}
+void free_walks(WalkBuffers& b, cudaStream_t st) {
+    cudaFreeAsync(b.ids, st);
+    cudaFreeAsync(b.dists, st);
+    cudaFreeAsync(b.hops, st);
+    cudaFreeAsync(b.evals, st);
+}
+
+void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t t0,
+                  uint32_t hop_limit, uint32_t cut, uint64_t seed, const uint64_t* d_states,
+                  WalkBuffers& wb, cudaStream_t st) {
+    GrArgs a{};
+    a.vec = idx->vec;
+    a.adj = idx->adj;
+    a.degcut = get_degcut(idx, cut, st);
+    a.queries = d_queries;
+    a.ld = idx->ld;
+    a.R = idx->R;
+    a.n = idx->n;
+    a.d = idx->d;
+    a.nq = nq;
+    a.t0 = t0;
+    a.hop_limit = hop_limit;
+    a.seed = seed;
+    a.walk_states = d_states;
+    a.walk_ids = wb.ids;
+    a.walk_dists = wb.dists;
+    a.walk_hops = wb.hops;
+    a.walk_evals = wb.evals;
+    a.work_counter = next_counter(idx, st);
+    a.dch = staging_dims(idx->ld);
+    Carve c;
+    a.off_bar = c.take(8, 8);
+    a.off_query = c.take(a.ld * 4);
+    a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
+    a.warp_smem = round_up(c.total, 128);
+    const size_t smem = (size_t)a.warp_smem * kGrWarps;
+    void (*kern)(GrArgs) = idx->metric == 0   ? greedy_walk_kernel<0>
+                           : idx->metric == 1 ? greedy_walk_kernel<1>
+                                              : greedy_walk_kernel<2>;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute(greedy)");
+    const int grid = grid_for(kern, kGrWarps * 32, smem, idx->sm_count, nq * t0, kGrWarps);
+    kern<<<grid, kGrWarps * 32, smem, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
+}
+
+void launch_greedy(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
+                   const tsdg_greedy_params* p, int mode, uint32_t* d_ids, float* d_dists,
+                   uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
+    (void)mode;
+    if (nq == 0) return;
+    WalkBuffers wb = alloc_walks(nq * p->t0, st);
+    launch_walks(idx, d_queries, nq, p->t0, p->hop_limit, p->lambda_cut, p->seed, nullptr, wb, st);
+    uint32_t npow2 = 32;
+    while (npow2 < p->t0 * 32) npow2 <<= 1;
+    const size_t smem = (size_t)npow2 * 8 + (kMergeThreads + 1) * 4;
+    cuda_check(cudaFuncSetAttribute(greedy_merge_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute(merge)");
+    greedy_merge_kernel<<<nq, kMergeThreads, smem, st>>>(wb.ids, wb.dists, wb.hops, wb.evals,
+                                                         p->t0, k, npow2, d_ids, d_dists,
+                                                         d_counts, d_stats);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "greedy_merge_kernel launch");
+    free_walks(wb, st);
+}
+
+void check_cosine_queries(const tsdg_gpu_index* idx, const float* queries, uint32_t nq) {
+    // require_metric_ready (vectors.cpp:83-95), applied to host query buffers.
+    if (idx->metric != TSDG_METRIC_COSINE || !queries) return;
+    for (uint32_t q = 0; q < nq; ++q) {
+        float sq = 0.0f;
+        const float* r = queries + (size_t)q * idx->d;
+        for (uint32_t i = 0; i < idx->d; ++i) sq += r[i] * r[i];
+        if (std::fabs(sq - 1.0f) > 1e-4f)
+            fail(TSDG_EINVAL, "Cosine requires unit-normalized vectors (row " + std::to_string(q) +
+                                  " has squared norm " + std::to_string(sq) +
+                                  "); pass the set through normalized_copy first");
+    }
+}
+
+template <class T>
+T* dev_alloc(size_t count, cudaStream_t st) {
+    T* p = nullptr;
+    if (count == 0) count = 1;
+    cuda_check(cudaMallocAsync(&p, sizeof(T) * count, st), "cudaMallocAsync");
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsdg_gpu_last_error(void) { return g_err.c_str(); }
+int tsdg_gpu_abi_version(void) { return TSDG_GPU_ABI_VERSION; }
+uint64_t tsdg_gpu_launch_count(void) { return g_launches.load(); }
+
+int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint64_t* offsets,
+                          const uint32_t* targets, const uint16_t* lambdas, int metric,
+                          int device, tsdg_gpu_index** out) {
+    return guarded([&] {
+        if (!out) fail(TSDG_EINVAL, "index_create: null out");
+        *out = nullptr;
+        if (d < 1) fail(TSDG_EINVAL, "index_create: d must be >= 1");
+        if (metric < 0 || metric > 2) fail(TSDG_EINVAL, "invalid metric");
+        if (n > 0 && (!base || !offsets || !targets || !lambdas))
+            fail(TSDG_EINVAL, "index_create: null input array");
+        auto idx = std::make_unique<tsdg_gpu_index>();
+        idx->device = device;
+        DeviceGuard dg(device);
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        idx->sm_count = prop.multiProcessorCount;
+        idx->n = n;
+        idx->d = d;
+        idx->ld = round_up(d, 4);
+        idx->metric = metric;
+        uint32_t maxdeg = 0;
+        for (uint32_t u = 0; u < n; ++u) {
+            if (offsets[u + 1] < offsets[u]) fail(TSDG_EINVAL, "index_create: offsets not monotone");
+            maxdeg = std::max<uint32_t>(maxdeg, (uint32_t)(offsets[u + 1] - offsets[u]));
+        }
+        idx->max_degree = maxdeg;
+        idx->R = std::max<uint32_t>(4, round_up(maxdeg, 4));
+        const uint64_t E = n ? offsets[n] : 0;
+        for (uint64_t j = 0; j < E; ++j)
+            if (targets[j] >= n) fail(TSDG_EINVAL, "index_create: edge target out of range");
+        cuda_check(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        // vectors, rows padded to ld floats (16-byte aligned for TMA bulk copies)
+        const size_t nv = (size_t)std::max<uint32_t>(n, 1) * idx->ld;
+        cuda_check(cudaMalloc(&idx->vec, nv * sizeof(float)), "cudaMalloc(vectors)");
+        if (n) {
+            if (idx->ld == d) {
+                cuda_check(cudaMemcpy(idx->vec, base, (size_t)n * d * 4, cudaMemcpyHostToDevice),
+                           "cudaMemcpy(vectors)");
+            } else {
+                cuda_check(cudaMemset(idx->vec, 0, nv * sizeof(float)), "cudaMemset");
+                cuda_check(cudaMemcpy2D(idx->vec, idx->ld * 4, base, d * 4, d * 4, n,
+                                        cudaMemcpyHostToDevice),
+                           "cudaMemcpy2D(vectors)");
+            }
+        }
+        // padded adjacency + lambdas + full degrees
+        const size_t na = (size_t)std::max<uint32_t>(n, 1) * idx->R;
+        std::vector<uint32_t> hadj(na, kInvalid);
+        std::vector<uint16_t> hlam(na, 0xFFFF);
+        std::vector<uint32_t> hdeg(std::max<uint32_t>(n, 1), 0);
+        for (uint32_t u = 0; u < n; ++u) {
+            const uint64_t b = offsets[u], e = offsets[u + 1];
+            hdeg[u] = (uint32_t)(e - b);
+            std::memcpy(&hadj[(size_t)u * idx->R], targets + b, (e - b) * 4);
+            std::memcpy(&hlam[(size_t)u * idx->R], lambdas + b, (e - b) * 2);
+        }
+        cuda_check(cudaMalloc(&idx->adj, na * 4), "cudaMalloc(adj)");
+        cuda_check(cudaMalloc(&idx->lam, na * 2), "cudaMalloc(lam)");
+        cuda_check(cudaMalloc(&idx->deg_full, hdeg.size() * 4), "cudaMalloc(deg)");
+        cuda_check(cudaMemcpy(idx->adj, hadj.data(), na * 4, cudaMemcpyHostToDevice), "cudaMemcpy(adj)");
+        cuda_check(cudaMemcpy(idx->lam, hlam.data(), na * 2, cudaMemcpyHostToDevice), "cudaMemcpy(lam)");
+        cuda_check(cudaMemcpy(idx->deg_full, hdeg.data(), hdeg.size() * 4, cudaMemcpyHostToDevice),
+                   "cudaMemcpy(deg)");
+        cuda_check(cudaMalloc(&idx->counters, kCounterSlots * 4), "cudaMalloc(counters)");
+        cuda_check(cudaMemset(idx->counters, 0, kCounterSlots * 4), "cudaMemset(counters)");
+        *out = idx.release();
+    });
+}
+
+int tsdg_gpu_index_create_from_file(const char* tsdg_path, const float* base, uint32_t n,
+                                    uint32_t d, int device, tsdg_gpu_index** out) {
+    tsdg_graph_header h{};
+    int rc = tsdg_read_tsdg_header(tsdg_path, &h);
+    if (rc) return rc;
+    if (h.n != n) {
+        g_err = "index_create_from_file: graph has " + std::to_string(h.n) + " nodes, base has " +
+                std::to_string(n);
+        return TSDG_EINVAL;
+    }
+    std::vector<uint64_t> off(h.n + 1);
+    std::vector<uint32_t> tgt(h.num_edges);
+    std::vector<uint16_t> lam(h.num_edges);
+    rc = tsdg_read_tsdg(tsdg_path, off.data(), tgt.data(), lam.data(), nullptr);
+    if (rc) return rc;
+    return tsdg_gpu_index_create(base, n, d, off.data(), tgt.data(), lam.data(), h.metric, device,
+                                 out);
+}
+
+int tsdg_gpu_index_destroy(tsdg_gpu_index* idx) {
+    return guarded([&] {
+        if (!idx) return;
+        DeviceGuard dg(idx->device);
+        cudaStreamSynchronize(idx->stream);
+        for (auto& kv : idx->degcut) cudaFree(kv.second);
+        cudaFree(idx->vec);
+        cudaFree(idx->adj);
+        cudaFree(idx->lam);
+        cudaFree(idx->deg_full);
+        cudaFree(idx->counters);
+        cudaStreamDestroy(idx->stream);
+        delete idx;
+    });
+}
+
+int tsdg_gpu_index_info(const tsdg_gpu_index* idx, uint32_t* n, uint32_t* d, int* metric,
+                        uint32_t* max_degree, int* device, uint32_t* row_stride,
+                        uint32_t* adj_stride) {
+    if (!idx) {
+        g_err = "index_info: null index";
+        return TSDG_EINVAL;
+    }
+    if (n) *n = idx->n;
+    if (d) *d = idx->d;
+    if (metric) *metric = idx->metric;
+    if (max_degree) *max_degree = idx->max_degree;
+    if (device) *device = idx->device;
+    if (row_stride) *row_stride = idx->ld;
+    if (adj_stride) *adj_stride = idx->R;
+    return TSDG_OK;
+}
+
+int tsdg_gpu_deg_cut(tsdg_gpu_index* idx, uint32_t lambda_cut, uint32_t* out) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "deg_cut: null index");
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        const uint32_t* dc = get_degcut(idx, lambda_cut, idx->stream);
+        if (out && idx->n) {
+            cuda_check(cudaMemcpyAsync(out, dc, sizeof(uint32_t) * idx->n, cudaMemcpyDeviceToHost,
+                                       idx->stream),
+                       "cudaMemcpyAsync(deg_cut)");
+        }
+        cuda_check(cudaStreamSynchronize(idx->stream), "cudaStreamSynchronize");
+    });
+}
+
+int tsdg_gpu_search_bestfirst_device(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
+                                     uint64_t query_index_base, const tsdg_bf_params* params,
+                                     int mode, uint32_t* d_ids, float* d_dists,
+                                     uint32_t* d_counts, tsdg_query_stats* d_stats,
+                                     void* stream) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "bestfirst_search: null index");
+        validate_bf(idx, params);
+        if (nq && (!d_queries || !d_ids)) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        launch_bestfirst(idx, d_queries, nq, query_index_base, params, mode, d_ids, d_dists,
+                         d_counts, d_stats, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                              uint64_t query_index_base, const tsdg_bf_params* params,
+                              int mode, uint32_t* ids, float* dists, uint32_t* counts,
+                              tsdg_query_stats* stats) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "bestfirst_search: null index");
+        validate_bf(idx, params);
+        if (nq && (!queries || !ids)) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
+        check_cosine_queries(idx, queries, nq);
+        if (nq == 0) return;
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        cudaStream_t st = idx->stream;
+        const uint32_t k = params->k;
+        float* dq = dev_alloc<float>((size_t)nq * idx->d, st);
+        uint32_t* di = dev_alloc<uint32_t>((size_t)nq * k, st);
+        float* dd = dev_alloc<float>((size_t)nq * k, st);
+        uint32_t* dc = dev_alloc<uint32_t>(nq, st);
+        tsdg_query_stats* ds = stats ? dev_alloc<tsdg_query_stats>(nq, st) : nullptr;
+        cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st),
+                   "cudaMemcpyAsync(queries)");
+        launch_bestfirst(idx, dq, nq, query_index_base, params, mode, di, dd, dc, ds, st);
+        cuda_check(cudaMemcpyAsync(ids, di, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+        if (dists)
+            cuda_check(cudaMemcpyAsync(dists, dd, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st),
+                       "D2H dists");
+        if (counts)
+            cuda_check(cudaMemcpyAsync(counts, dc, (size_t)nq * 4, cudaMemcpyDeviceToHost, st),
+                       "D2H counts");
+        if (stats)
+            cuda_check(cudaMemcpyAsync(stats, ds, (size_t)nq * sizeof(tsdg_query_stats),
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H stats");
+        cudaFreeAsync(dq, st);
+        cudaFreeAsync(di, st);
+        cudaFreeAsync(dd, st);
+        cudaFreeAsync(dc, st);
+        if (ds) cudaFreeAsync(ds, st);
+        cuda_check(cudaStreamSynchronize(st), "bestfirst_search");
+    });
+}
+
+int tsdg_gpu_search_greedy_device(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
+                                  uint32_t k, const tsdg_greedy_params* params, int mode,
+                                  uint32_t* d_ids, float* d_dists, uint32_t* d_counts,
+                                  tsdg_query_stats* d_stats, void* stream) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "small_batch_search: null index");
+        validate_greedy(idx, k, params);
+        if (nq && (!d_queries || !d_ids)) fail(TSDG_EINVAL, "small_batch_search: null buffer");
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        launch_greedy(idx, d_queries, nq, k, params, mode, d_ids, d_dists, d_counts, d_stats,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t nq, uint32_t k,
+                           const tsdg_greedy_params* params, int mode, uint32_t* ids,
+                           float* dists, uint32_t* counts, tsdg_query_stats* stats) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "small_batch_search: null index");
+        validate_greedy(idx, k, params);
+        if (nq && (!queries || !ids)) fail(TSDG_EINVAL, "small_batch_search: null buffer");
+        check_cosine_queries(idx, queries, nq);
+        if (nq == 0) return;
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        cudaStream_t st = idx->stream;
+        float* dq = dev_alloc<float>((size_t)nq * idx->d, st);
+        uint32_t* di = dev_alloc<uint32_t>((size_t)nq * k, st);
+        float* dd = dev_alloc<float>((size_t)nq * k, st);
+        uint32_t* dc = dev_alloc<uint32_t>(nq, st);
+        tsdg_query_stats* ds = stats ? dev_alloc<tsdg_query_stats>(nq, st) : nullptr;
+        cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st),
+                   "cudaMemcpyAsync(queries)");
+        launch_greedy(idx, dq, nq, k, params, mode, di, dd, dc, ds, st);
+        cuda_check(cudaMemcpyAsync(ids, di, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+        if (dists)
+            cuda_check(cudaMemcpyAsync(dists, dd, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st),
+                       "D2H dists");
+        if (counts)
+            cuda_check(cudaMemcpyAsync(counts, dc, (size_t)nq * 4, cudaMemcpyDeviceToHost, st),
+                       "D2H counts");
+        if (stats)
+            cuda_check(cudaMemcpyAsync(stats, ds, (size_t)nq * sizeof(tsdg_query_stats),
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H stats");
+        cudaFreeAsync(dq, st);
+        cudaFreeAsync(di, st);
+        cudaFreeAsync(dd, st);
+        cudaFreeAsync(dc, st);
+        if (ds) cudaFreeAsync(ds, st);
+        cuda_check(cudaStreamSynchronize(st), "small_batch_search");
+    });
+}
+
+int tsdg_gpu_greedy_once(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                         const uint64_t* rng_states, uint32_t hop_limit, uint32_t lambda_cut,
+                         uint32_t* ids32, float* dists32, tsdg_query_stats* stats) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "greedy_search_once: null index");
+        if (lambda_cut < 1) fail(TSDG_EINVAL, "greedy_search_once: lambda_cut must be >= 1");
+        if (hop_limit < 1) fail(TSDG_EINVAL, "greedy_search_once: hop limit must be >= 1");
+        if (idx->n == 0) fail(TSDG_EINVAL, "select_start: empty graph");
+        if (nq == 0) return;
+        if (!queries || !rng_states || !ids32) fail(TSDG_EINVAL, "greedy_search_once: null buffer");
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        cudaStream_t st = idx->stream;
+        float* dq = dev_alloc<float>((size_t)nq * idx->d, st);
+        uint64_t* dst = dev_alloc<uint64_t>(nq, st);
+        cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(dst, rng_states, (size_t)nq * 8, cudaMemcpyHostToDevice, st), "H2D");
+        WalkBuffers wb = alloc_walks(nq, st);
+        launch_walks(idx, dq, nq, 1, hop_limit, lambda_cut, 0, dst, wb, st);
+        cuda_check(cudaMemcpyAsync(ids32, wb.ids, (size_t)nq * 32 * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (dists32)
+            cuda_check(cudaMemcpyAsync(dists32, wb.dists, (size_t)nq * 32 * 4, cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        std::vector<uint32_t> h(nq), e(nq);
+        cuda_check(cudaMemcpyAsync(h.data(), wb.hops, (size_t)nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(e.data(), wb.evals, (size_t)nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        free_walks(wb, st);
+        cudaFreeAsync(dq, st);
+        cudaFreeAsync(dst, st);
+        cuda_check(cudaStreamSynchronize(st), "greedy_search_once");
+        if (stats) {
+            for (uint32_t q = 0; q < nq; ++q) {
+                stats[q].hops = h[q];
+                stats[q].distance_evals = e[q];
+                stats[q].queue_evictions = 0;
+                stats[q].edges_examined = e[q] - 32;
+            }
+        }
+    });
+}
+
+int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
+                                 const uint32_t* d_counts, const uint64_t* shard_base,
+                                 uint32_t shards, uint32_t nq, uint32_t k, uint32_t* d_out_ids,
+                                 float* d_out_dists, uint32_t* d_out_counts, void* stream) {
+    return guarded([&] {
+        if (shards < 1 || k < 1) fail(TSDG_EINVAL, "merge_shards: need shards >= 1 and k >= 1");
+        if (nq == 0) return;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint32_t npow2 = 32;
+        while (npow2 < shards * k) npow2 <<= 1;
+        const size_t smem = (size_t)npow2 * 8;
+        if (smem > 200 * 1024) fail(TSDG_EINVAL, "merge_shards: shards * k too large");
+        uint64_t* dbase = dev_alloc<uint64_t>(shards, st);
+        cuda_check(cudaMemcpyAsync(dbase, shard_base, shards * 8, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaFuncSetAttribute(merge_shards_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                   "cudaFuncSetAttribute(merge_shards)");
+        merge_shards_kernel<<<nq, kMergeThreads, smem, st>>>(d_ids, d_dists, d_counts, dbase,
+                                                             shards, nq, k, npow2, d_out_ids,
+                                                             d_out_dists, d_out_counts);
+        g_launches++;
+        cuda_check(cudaGetLastError(), "merge_shards_kernel launch");
+        cudaFreeAsync(dbase, st);
+    });
+}
+
+}  // extern "C"
