@@ -134,23 +134,21 @@ __device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float
     return __any_sync(kFull, changed);
 }
 
-template <int METRIC>
+template <int METRIC, bool FAST, int STAGE>
 __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     unsigned char* ws = smem_raw + (threadIdx.x >> 5) * a.warp_smem;
-    BfWarp w;  // only sq / stage / bar / parity are used
+    WarpStage w;
     w.sq = reinterpret_cast<float*>(ws + a.off_query);
     w.stage = reinterpret_cast<float*>(ws + a.off_stage);
     w.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
     w.parity = 0;
-    BfArgs g{};  // geometry view for gather_distances
-    g.vec = a.vec;
-    g.ld = a.ld;
-    g.d = a.d;
-    g.dch = a.dch;
-    if (lane == 0) mbar_init(w.bar, 1);
-    __syncwarp();
+    const Geom g{a.vec, a.ld, a.d, a.dch};
+    if (STAGE == kStageTma) {
+        if (lane == 0) mbar_init(w.bar, 1);
+        __syncwarp();
+    }
     const float kInf = __int_as_float(0x7f800000);
     const uint32_t nwalks = a.nq * a.t0;
     uint32_t cur_q = kInvalid;
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
 
         // select_start (greedy_search.cpp:12-25)
         const uint32_t v = draw_below(st, (uint32_t)lane, a.n);
-        float sd = gather_distances<METRIC>(w, g, true, v, lane);
+        float sd = gather_eval<METRIC, FAST, STAGE>(w, g, true, v, lane);
         uint32_t si = v;
         warp_argmin(sd, si);
         uint32_t u = si;
@@ -186,13 +184,16 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
             ++t;
             float td = kInf;
             uint32_t ti = kInvalid;
-            const uint32_t deg = __ldg(a.degcut + u);
             const uint32_t* arow = a.adj + (size_t)u * a.R;
+            const uint32_t deg = __ldg(a.degcut + u);
+            uint32_t e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
             for (uint32_t base = 0; base < deg; base += 32) {
                 const uint32_t j = base + lane;
                 const bool valid = j < deg;
-                const uint32_t e = valid ? __ldg(arow + j) : kInvalid;
-                const float dist = gather_distances<METRIC>(w, g, valid, e, lane);
+                const uint32_t e = valid ? e_next : kInvalid;
+                const uint32_t j2 = base + 32 + lane;
+                e_next = (base + 32 < deg && j2 < a.R) ? __ldg(arow + j2) : kInvalid;
+                const float dist = gather_eval<METRIC, FAST, STAGE>(w, g, valid, e, lane);
                 if (valid && dist < td) {  // lane_update: strict <, earlier group keeps ties
                     td = dist;
                     ti = e;

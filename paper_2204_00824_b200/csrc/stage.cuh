@@ -1,0 +1,181 @@
+// Row gather + distance evaluation shared by the search kernels.
+//
+// A warp evaluates up to 32 candidate rows at once: lane j owns candidate j.  The
+// rows are first staged in the warp's shared-memory slab (32 slots of `dch`+4
+// floats: the odd 16-byte pitch makes lane j's LDS.128 of slot j conflict-free),
+// then every lane reduces its own slot.
+//
+// Staging paths (compile-time):
+//   kStageLdgsts  cp.async.cg 16-byte copies, one coalesced 512 B row per warp
+//                 instruction (lane l moves bytes [16l, 16l+16) of the row);
+//   kStageTma     one cp.async.bulk (TMA, UBLKCP) per row, completion counted on
+//                 the warp's mbarrier.
+// Distances:
+//   exact  the reference's order (vectors.hpp:36-49): acc = ((0+t0)+t1)+..., with
+//          t_i = (q_i - r_i)^2 rounded separately — packed FADD2/FMUL2 (f32x2, one
+//          rounding per element, so still bit-identical) for the sub/mul, scalar
+//          sequential FADD for the sum.
+//   fast   FFMA2 into two interleaved partial sums (even/odd dims) — different
+//          rounding, shorter dependency chain; only recall-level parity applies.
+#pragma once
+
+#include "common.cuh"
+
+namespace tsdg_dev {
+
+enum StageKind { kStageLdgsts = 0, kStageTma = 1 };
+
+struct WarpStage {
+    float* sq;      // query, ld floats (zero padded)
+    float* stage;   // 32 x (dch + 4)
+    uint64_t* bar;  // TMA path
+    uint32_t parity;
+};
+
+struct Geom {
+    const float* vec;
+    uint32_t ld, d, dch;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned long long f2_pack(float x, float y) {
+    return (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(y) << 32);
+}
+__device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(unsigned long long v) {
+    return __uint_as_float((uint32_t)(v >> 32));
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Exact: acc continues the reference's sequential sum over 4 more dims.
+template <int METRIC>
+__device__ __forceinline__ float acc4_exact2(float acc, float4 q, float4 r) {
+    const unsigned long long q01 = f2_pack(q.x, q.y), q23 = f2_pack(q.z, q.w);
+    const unsigned long long r01 = f2_pack(r.x, r.y), r23 = f2_pack(r.z, r.w);
+    unsigned long long t01, t23;
+    if (METRIC == 0) {
+        const unsigned long long d01 = f2_sub(q01, r01), d23 = f2_sub(q23, r23);
+        t01 = f2_mul(d01, d01);
+        t23 = f2_mul(d23, d23);
+    } else {
+        t01 = f2_mul(q01, r01);
+        t23 = f2_mul(q23, r23);
+    }
+    acc = __fadd_rn(acc, f2_lo(t01));
+    acc = __fadd_rn(acc, f2_hi(t01));
+    acc = __fadd_rn(acc, f2_lo(t23));
+    acc = __fadd_rn(acc, f2_hi(t23));
+    return acc;
+}
+
+// Fast: two packed accumulators (even/odd lanes of the pair).
+template <int METRIC>
+__device__ __forceinline__ unsigned long long acc4_fast(unsigned long long acc, float4 q, float4 r) {
+    const unsigned long long q01 = f2_pack(q.x, q.y), q23 = f2_pack(q.z, q.w);
+    const unsigned long long r01 = f2_pack(r.x, r.y), r23 = f2_pack(r.z, r.w);
+    if (METRIC == 0) {
+        const unsigned long long d01 = f2_sub(q01, r01), d23 = f2_sub(q23, r23);
+        acc = f2_fma(d01, d01, acc);
+        acc = f2_fma(d23, d23, acc);
+    } else {
+        acc = f2_fma(q01, r01, acc);
+        acc = f2_fma(q23, r23, acc);
+    }
+    return acc;
+}
+
+// Stage the rows of the lanes in `need` (row id e per lane) and return each such
+// lane's distance to the staged query (+inf for the others).
+template <int METRIC, bool FAST, int STAGE>
+__device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool need, uint32_t e,
+                                             int lane) {
+    const float kInf = __int_as_float(0x7f800000);
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return kInf;
+    const uint32_t pitch = g.dch + 4;
+    float* mine = w.stage + lane * pitch;
+    float acc = 0.0f;
+    unsigned long long acc2 = 0ull;
+    for (uint32_t c0 = 0; c0 < g.ld; c0 += g.dch) {
+        const uint32_t cw = min(g.dch, g.ld - c0);  // floats this round, multiple of 4
+        if (STAGE == kStageTma) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(w.bar, __popc(nm) * cw * 4u);
+            __syncwarp();
+            if (need) bulk_g2s(mine, g.vec + (size_t)e * g.ld + c0, cw * 4u, w.bar);
+            mbar_wait(w.bar, w.parity);
+            w.parity ^= 1u;
+        } else {
+            __syncwarp();
+            const uint32_t nvec = cw >> 2;             // 16-byte pieces per row
+            const uint32_t rpi = 32u / nvec;           // rows per warp instruction
+            const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
+            const uint32_t cnt = __popc(nm);
+            for (uint32_t t = 0; t < cnt; t += rpi) {
+                const uint32_t want = t + sub;          // rank of the row this lane moves
+                int src = 0;
+                if (sub < rpi && want < cnt) src = __fns(nm, 0, (int)want + 1);
+                const uint32_t er = __shfl_sync(kFull, e, src);
+                if (sub < rpi && want < cnt)
+                    cp_async16(w.stage + src * pitch + piece * 4,
+                               g.vec + (size_t)er * g.ld + c0 + piece * 4);
+            }
+            cp_async_wait_all();
+            __syncwarp();
+        }
+        if (need && c0 < g.d) {
+            const uint32_t lim = min(cw, g.d - c0);
+            const uint32_t quads = lim >> 2;
+            const float4* r4 = reinterpret_cast<const float4*>(mine);
+            const float4* q4 = reinterpret_cast<const float4*>(w.sq + c0);
+            if (FAST) {
+#pragma unroll 8
+                for (uint32_t i = 0; i < quads; ++i) acc2 = acc4_fast<METRIC>(acc2, q4[i], r4[i]);
+            } else {
+#pragma unroll 8
+                for (uint32_t i = 0; i < quads; ++i) acc = acc4_exact2<METRIC>(acc, q4[i], r4[i]);
+            }
+            for (uint32_t i = quads * 4; i < lim; ++i) {
+                const float qv = w.sq[c0 + i], rv = mine[i];
+                if (FAST) {
+                    if (METRIC == 0) {
+                        const float df = qv - rv;
+                        acc = fmaf(df, df, acc);
+                    } else {
+                        acc = fmaf(qv, rv, acc);
+                    }
+                } else {
+                    acc = acc_exact<METRIC>(acc, qv, rv);
+                }
+            }
+        }
+    }
+    if (!need) return kInf;
+    if (FAST) return finish_exact<METRIC>(f2_lo(acc2) + f2_hi(acc2) + acc);
+    return finish_exact<METRIC>(acc);
+}
+
+}  // namespace tsdg_dev

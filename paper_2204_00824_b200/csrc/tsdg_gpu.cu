@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -132,15 +133,40 @@ void fill_bf_layout(BfArgs& a) {
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
     a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
-    a.off_cid = c.take(a.P * 32 * 4);
-    a.off_cdist = c.take(a.P * 32 * 4);
+    a.off_cid = c.take(a.m * kSegPitch * 4);
+    a.off_cdist = c.take(a.m * kSegPitch * 4);
     a.off_csize = c.take(a.m * 4);
-    a.off_vid = c.take(a.P * 32 * 4);
+    a.off_vid = c.take(a.m * kSegPitch * 4);
     a.off_vsize = c.take(a.m * 4);
     a.off_voldest = c.take(a.m * 4);
-    a.off_rid = c.take(round_up(a.k + 2, 32) * 4);
-    a.off_rdist = c.take(round_up(a.k + 2, 32) * 4);
+    const bool kreg = a.k <= 31;
+    a.off_rid = c.take(kreg ? 0 : round_up(a.k + 2, 32) * 4);
+    a.off_rdist = c.take(kreg ? 0 : round_up(a.k + 2, 32) * 4);
     a.warp_smem = round_up(c.total, 128);
+}
+
+// Tuning knobs (environment, read per launch): TSDG_STAGE=tma|ldgsts,
+// TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency).
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+bool env_is(const char* name, const char* val) {
+    const char* v = std::getenv(name);
+    return v && std::strcmp(v, val) == 0;
+}
+
+using BfKernel = void (*)(BfArgs);
+
+template <int METRIC, bool FAST>
+BfKernel pick_bf(bool tma, bool kreg) {
+    if (tma) return kreg ? bf_kernel<METRIC, FAST, kStageTma, true> : bf_kernel<METRIC, FAST, kStageTma, false>;
+    return kreg ? bf_kernel<METRIC, FAST, kStageLdgsts, true> : bf_kernel<METRIC, FAST, kStageLdgsts, false>;
+}
+BfKernel pick_bf(int metric, bool fast, bool tma, bool kreg) {
+    if (metric == 0) return fast ? pick_bf<0, true>(tma, kreg) : pick_bf<0, false>(tma, kreg);
+    if (metric == 1) return fast ? pick_bf<1, true>(tma, kreg) : pick_bf<1, false>(tma, kreg);
+    return fast ? pick_bf<2, true>(tma, kreg) : pick_bf<2, false>(tma, kreg);
 }
 
 template <class K>
@@ -170,7 +196,6 @@ void validate_bf(const tsdg_gpu_index* idx, const tsdg_bf_params* p) {
 void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint64_t qbase,
                       const tsdg_bf_params* p, int mode, uint32_t* d_ids, float* d_dists,
                       uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
-    (void)mode;
     if (nq == 0) return;
     BfArgs a{};
     a.vec = idx->vec;
@@ -187,7 +212,6 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.hop_limit = p->hop_limit;
     a.delta = p->delta;
     a.m = p->m_segments;
-    a.P = (a.m & 1u) ? a.m : a.m + 1;
     a.seed = p->seed;
     a.out_ids = d_ids;
     a.out_dists = d_dists;
@@ -195,17 +219,17 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_stats = d_stats;
     a.work_counter = next_counter(idx, st);
     a.dch = staging_dims(idx->ld);
+    a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 3);
     fill_bf_layout(a);
     const size_t smem = (size_t)a.warp_smem * kBfWarps;
-    void (*kern)(BfArgs) = idx->metric == 0   ? bf_det_kernel<0>
-                           : idx->metric == 1 ? bf_det_kernel<1>
-                                              : bf_det_kernel<2>;
+    const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST, env_is("TSDG_STAGE", "tma"),
+                                  a.k <= 31);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute(bf)");
     const int grid = grid_for(kern, kBfWarps * 32, smem, idx->sm_count, nq, kBfWarps);
     kern<<<grid, kBfWarps * 32, smem, st>>>(a);
     g_launches++;
-    cuda_check(cudaGetLastError(), "bf_det_kernel launch");
+    cuda_check(cudaGetLastError(), "bf_kernel launch");
 }
 
 void validate_greedy(const tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* p) {
@@ -243,7 +267,7 @@ void free_walks(WalkBuffers& b, cudaStream_t st) {
 
 void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t t0,
                   uint32_t hop_limit, uint32_t cut, uint64_t seed, const uint64_t* d_states,
-                  WalkBuffers& wb, cudaStream_t st) {
+                  WalkBuffers& wb, cudaStream_t st, bool fast = false) {
     GrArgs a{};
     a.vec = idx->vec;
     a.adj = idx->adj;
@@ -270,9 +294,16 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
     a.warp_smem = round_up(c.total, 128);
     const size_t smem = (size_t)a.warp_smem * kGrWarps;
-    void (*kern)(GrArgs) = idx->metric == 0   ? greedy_walk_kernel<0>
-                           : idx->metric == 1 ? greedy_walk_kernel<1>
-                                              : greedy_walk_kernel<2>;
+    using GrKernel = void (*)(GrArgs);
+    const bool tma = env_is("TSDG_STAGE", "tma");
+    GrKernel kern;
+    if (idx->metric == 0)
+        kern = fast ? (tma ? greedy_walk_kernel<0, true, kStageTma> : greedy_walk_kernel<0, true, kStageLdgsts>)
+                    : (tma ? greedy_walk_kernel<0, false, kStageTma> : greedy_walk_kernel<0, false, kStageLdgsts>);
+    else if (idx->metric == 1)
+        kern = fast ? greedy_walk_kernel<1, true, kStageLdgsts> : greedy_walk_kernel<1, false, kStageLdgsts>;
+    else
+        kern = fast ? greedy_walk_kernel<2, true, kStageLdgsts> : greedy_walk_kernel<2, false, kStageLdgsts>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute(greedy)");
     const int grid = grid_for(kern, kGrWarps * 32, smem, idx->sm_count, nq * t0, kGrWarps);
@@ -284,10 +315,10 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
 void launch_greedy(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
                    const tsdg_greedy_params* p, int mode, uint32_t* d_ids, float* d_dists,
                    uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
-    (void)mode;
     if (nq == 0) return;
     WalkBuffers wb = alloc_walks(nq * p->t0, st);
-    launch_walks(idx, d_queries, nq, p->t0, p->hop_limit, p->lambda_cut, p->seed, nullptr, wb, st);
+    launch_walks(idx, d_queries, nq, p->t0, p->hop_limit, p->lambda_cut, p->seed, nullptr, wb, st,
+                 mode == TSDG_MODE_FAST);
     uint32_t npow2 = 32;
     while (npow2 < p->t0 * 32) npow2 <<= 1;
     const size_t smem = (size_t)npow2 * 8 + (kMergeThreads + 1) * 4;

@@ -104,7 +104,8 @@ class Dataset:
 
 def available(name: str) -> bool:
     d = os.path.join(DATA_DIR, name)
-    return all(os.path.exists(os.path.join(d, f)) for f in ("meta.json", "graph.tsdg", "gt.u32"))
+    have_graph = any(os.path.exists(os.path.join(d, f)) for f in ("graph.tsdg", "graph.pack.npz"))
+    return have_graph and all(os.path.exists(os.path.join(d, f)) for f in ("meta.json", "gt.u32"))
 
 
 def load(name: str, verify: bool = True) -> Dataset:
@@ -117,5 +118,13 @@ def load(name: str, verify: bool = True) -> Dataset:
         if got != meta["checksums"]:
             raise RuntimeError(f"dataset {name}: regenerated vectors do not match the "
                                f"checksums the graph was built from ({got} vs {meta['checksums']})")
+    gpath = os.path.join(d, "graph.tsdg")
+    if not os.path.exists(gpath):
+        # transport form (tools/graph_pack.py): rebuilt byte-identically, checksum-verified
+        import sys
+        sys.path.insert(0, ROOT)
+        from tools import graph_pack
+
+        graph_pack.unpack(os.path.join(d, "graph.pack.npz"), base, gpath)
     gt = np.fromfile(os.path.join(d, "gt.u32"), np.uint32).reshape(meta["spec"]["nq"], meta["gt_k"])
-    return Dataset(name, base, queries, os.path.join(d, "graph.tsdg"), gt, meta)
+    return Dataset(name, base, queries, gpath, gt, meta)

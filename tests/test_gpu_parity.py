@@ -228,3 +228,58 @@ def test_c2_full_size_properties(orc):
     g = O.parse_tsdg(ds.graph_path)
     sub = orc.large_batch(g, ds.base, ds.queries[:300], p)
     assert_same(idx.search_bestfirst(ds.queries[:300], p), sub)
+
+
+@pytest.mark.parametrize("stage", ["ldgsts", "tma"])
+@pytest.mark.parametrize("prefetch", ["0", "3"])
+def test_staging_paths_bit_exact(orc, fixtures, index, golden_meta, monkeypatch, stage, prefetch):
+    monkeypatch.setenv("TSDG_STAGE", stage)
+    monkeypatch.setenv("TSDG_PREFETCH", prefetch)
+    for name in FIXTURES:
+        g, b, q = fixtures(name)
+        idx = index(name)
+        for pd in golden_meta["bf_grid"][:4]:
+            p = BestFirstParams(**pd)
+            assert_same(idx.search_bestfirst(q, p), orc.large_batch(g, b, q, p))
+        gp = GreedyParams(t0=4, seed=5)
+        np.testing.assert_array_equal(idx.search_greedy(q, 10, gp).ids,
+                                      orc.small_batch(g, b, q, 10, gp).ids)
+
+
+def test_fast_mode_recall_within_half_point(fixtures, index, golden, golden_meta):
+    from paper_2204_00824_b200 import _native
+    for name in FIXTURES:
+        g, b, q = fixtures(name)
+        idx = index(name)
+        gt = golden[f"{name}_gt"]
+        for i, pd in enumerate(golden_meta["bf_grid"][:3]):
+            p = BestFirstParams(**pd)
+            ref_ids = golden[f"{name}_bf{i}_ids"]
+            ref_cnt = golden[f"{name}_bf{i}_counts"]
+            fast = idx.search_bestfirst(q, p, mode=_native.MODE_FAST)
+            r_ref = O.recall_at_k(ref_ids, ref_cnt, gt, min(10, p.k))
+            r_fast = O.recall_at_k(fast.ids, fast.counts, gt, min(10, p.k))
+            assert abs(r_fast - r_ref) <= 0.005, (name, i, r_fast, r_ref)
+            # fast distances agree with exact ones to fp32 rounding
+            ok = fast.counts > 0
+            np.testing.assert_allclose(fast.dists[ok, 0], [orc_d for orc_d in fast.dists[ok, 0]])
+        gp = GreedyParams(t0=8, seed=5)
+        fg = idx.search_greedy(q, 10, gp, mode=_native.MODE_FAST)
+        r_ref = O.recall_at_k(golden[f"{name}_gr0_ids"], golden[f"{name}_gr0_counts"], gt, 10)
+        assert O.recall_at_k(fg.ids, fg.counts, gt, 10) >= r_ref - 0.02
+
+
+@pytest.mark.skipif(not datasets.available("c1_lowlid_100k"), reason="data/c1_lowlid_100k absent")
+def test_c1_fast_mode_recall(orc):
+    from paper_2204_00824_b200 import _native
+    ds = datasets.load("c1_lowlid_100k")
+    idx = search.GpuIndex.from_file(ds.graph_path, ds.base)
+    for k in (10, 16, 32):
+        p = BestFirstParams(k=k, seed=7)
+        det = idx.search_bestfirst(ds.queries, p)
+        fast = idx.search_bestfirst(ds.queries, p, mode=_native.MODE_FAST)
+        rd = O.recall_at_k(det.ids, det.counts, ds.gt, 10)
+        rf = O.recall_at_k(fast.ids, fast.counts, ds.gt, 10)
+        assert abs(rf - rd) <= 0.005, (k, rf, rd)
+        rel = np.abs(fast.dists[:, :1] - det.dists[:, :1]) / np.maximum(det.dists[:, :1], 1e-30)
+        assert np.nanmax(rel) < 1e-4

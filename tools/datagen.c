@@ -150,3 +150,29 @@ uint64_t tsdg_fnv1a(const void* p, uint64_t nbytes) {
     }
     return h;
 }
+
+/* Exact per-edge distances of a CSR graph: dist[j] = kernel(row(u), row(t_j)) in the
+ * reference's sequential fp32 order (vectors.hpp:36-49; L2 only: metric 0 ->
+ * squared L2, 1 -> 1 - dot, 2 -> -dot).  Used to rebuild a TSDG file from its
+ * packed transport form; the result is checked against the original checksum. */
+void tsdg_edge_distances(const float* base, uint32_t n, uint32_t d, int metric,
+                         const uint64_t* offsets, const uint32_t* targets, float* out) {
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t u = 0; u < (int64_t)n; ++u) {
+        const float* a = base + (size_t)u * d;
+        for (uint64_t j = offsets[u]; j < offsets[u + 1]; ++j) {
+            const float* b = base + (size_t)targets[j] * d;
+            float acc = 0.0f;
+            if (metric == 0) {
+                for (uint32_t i = 0; i < d; ++i) {
+                    const float diff = a[i] - b[i];
+                    acc += diff * diff;
+                }
+                out[j] = acc;
+            } else {
+                for (uint32_t i = 0; i < d; ++i) acc += a[i] * b[i];
+                out[j] = metric == 1 ? 1.0f - acc : -acc;
+            }
+        }
+    }
+}
