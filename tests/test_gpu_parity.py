@@ -260,9 +260,6 @@ def test_fast_mode_recall_within_half_point(fixtures, index, golden, golden_meta
             r_ref = O.recall_at_k(ref_ids, ref_cnt, gt, min(10, p.k))
             r_fast = O.recall_at_k(fast.ids, fast.counts, gt, min(10, p.k))
             assert abs(r_fast - r_ref) <= 0.005, (name, i, r_fast, r_ref)
-            # fast distances agree with exact ones to fp32 rounding
-            ok = fast.counts > 0
-            np.testing.assert_allclose(fast.dists[ok, 0], [orc_d for orc_d in fast.dists[ok, 0]])
         gp = GreedyParams(t0=8, seed=5)
         fg = idx.search_greedy(q, 10, gp, mode=_native.MODE_FAST)
         r_ref = O.recall_at_k(golden[f"{name}_gr0_ids"], golden[f"{name}_gr0_counts"], gt, 10)
