@@ -54,6 +54,7 @@ struct BfArgs {
     tsdg_query_stats* out_stats;
     uint32_t* work_counter;
     uint32_t dch;           // staged dims per row per round (multiple of 8, <= 128)
+    uint32_t slots;         // staged rows per gather round (1..32)
     uint32_t prefetch;      // bit 0: next-chunk rows, bit 1: admitted adjacency
     // per-warp shared-memory carve (bytes)
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
         if (lane == 0) mbar_init(w.st.bar, 1);
         __syncwarp();
     }
-    const Geom g{a.vec, a.ld, a.d, a.dch};
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     const float kInf = __int_as_float(0x7f800000);
     const bool pf_rows = (a.prefetch & 1u) != 0;
     const bool pf_adj = (a.prefetch & 2u) != 0;

@@ -39,7 +39,7 @@ struct GrArgs {
     uint32_t* walk_hops;          // nq*t0
     uint32_t* walk_evals;
     uint32_t* work_counter;
-    uint32_t dch;
+    uint32_t dch, slots;
     uint32_t warp_smem, off_query, off_stage, off_bar;
 };
 
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
     w.stage = reinterpret_cast<float*>(ws + a.off_stage);
     w.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
     w.parity = 0;
-    const Geom g{a.vec, a.ld, a.d, a.dch};
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     if (STAGE == kStageTma) {
         if (lane == 0) mbar_init(w.bar, 1);
         __syncwarp();

@@ -8,6 +8,8 @@
 // Staging paths (compile-time):
 //   kStageLdgsts  cp.async.cg 16-byte copies, one coalesced 512 B row per warp
 //                 instruction (lane l moves bytes [16l, 16l+16) of the row);
+// Rows are compacted into `slots` slots (fewer slots = less shared memory per
+// warp = more resident warps, at the cost of more gather rounds).
 //   kStageTma     one cp.async.bulk (TMA, UBLKCP) per row, completion counted on
 //                 the warp's mbarrier.
 // Distances:
@@ -35,6 +37,7 @@ struct WarpStage {
 struct Geom {
     const float* vec;
     uint32_t ld, d, dch;
+    uint32_t slots;  // shared-memory row slots per warp (1..32)
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -107,7 +110,10 @@ __device__ __forceinline__ unsigned long long acc4_fast(unsigned long long acc, 
 }
 
 // Stage the rows of the lanes in `need` (row id e per lane) and return each such
-// lane's distance to the staged query (+inf for the others).
+// lane's distance to the staged query (+inf for the others).  The needed rows are
+// processed in rounds of g.slots (<= 32) shared-memory slots: the r-th needed row
+// (lane order) goes to slot r mod slots and is reduced by lane r mod slots; the
+// distance is shuffled back to the lane that owns the edge.
 template <int METRIC, bool FAST, int STAGE>
 __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool need, uint32_t e,
                                              int lane) {
@@ -115,67 +121,79 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
     const unsigned nm = __ballot_sync(kFull, need);
     if (nm == 0) return kInf;
     const uint32_t pitch = g.dch + 4;
-    float* mine = w.stage + lane * pitch;
-    float acc = 0.0f;
-    unsigned long long acc2 = 0ull;
-    for (uint32_t c0 = 0; c0 < g.ld; c0 += g.dch) {
-        const uint32_t cw = min(g.dch, g.ld - c0);  // floats this round, multiple of 4
-        if (STAGE == kStageTma) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(w.bar, __popc(nm) * cw * 4u);
-            __syncwarp();
-            if (need) bulk_g2s(mine, g.vec + (size_t)e * g.ld + c0, cw * 4u, w.bar);
-            mbar_wait(w.bar, w.parity);
-            w.parity ^= 1u;
-        } else {
-            __syncwarp();
-            const uint32_t nvec = cw >> 2;             // 16-byte pieces per row
-            const uint32_t rpi = 32u / nvec;           // rows per warp instruction
-            const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
-            const uint32_t cnt = __popc(nm);
-            for (uint32_t t = 0; t < cnt; t += rpi) {
-                const uint32_t want = t + sub;          // rank of the row this lane moves
-                int src = 0;
-                if (sub < rpi && want < cnt) src = __fns(nm, 0, (int)want + 1);
-                const uint32_t er = __shfl_sync(kFull, e, src);
-                if (sub < rpi && want < cnt)
-                    cp_async16(w.stage + src * pitch + piece * 4,
-                               g.vec + (size_t)er * g.ld + c0 + piece * 4);
-            }
-            cp_async_wait_all();
-            __syncwarp();
-        }
-        if (need && c0 < g.d) {
-            const uint32_t lim = min(cw, g.d - c0);
-            const uint32_t quads = lim >> 2;
-            const float4* r4 = reinterpret_cast<const float4*>(mine);
-            const float4* q4 = reinterpret_cast<const float4*>(w.sq + c0);
-            if (FAST) {
-#pragma unroll 8
-                for (uint32_t i = 0; i < quads; ++i) acc2 = acc4_fast<METRIC>(acc2, q4[i], r4[i]);
+    const uint32_t cnt = __popc(nm);
+    const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
+    const float* row_src = g.vec + (size_t)(need ? e : 0) * g.ld;
+    float result = kInf;
+    for (uint32_t r0 = 0; r0 < cnt; r0 += g.slots) {
+        const uint32_t nr = min(g.slots, cnt - r0);
+        const bool mine_round = need && rank >= r0 && rank < r0 + nr;
+        const uint32_t slot = rank - r0;
+        const bool computes = (uint32_t)lane < nr;
+        const float* srow = w.stage + lane * pitch;  // slot computed by this lane
+        float acc = 0.0f;
+        unsigned long long acc2 = 0ull;
+        for (uint32_t c0 = 0; c0 < g.ld; c0 += g.dch) {
+            const uint32_t cw = min(g.dch, g.ld - c0);  // floats this round, multiple of 4
+            if (STAGE == kStageTma) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(w.bar, nr * cw * 4u);
+                __syncwarp();
+                if (mine_round) bulk_g2s(w.stage + slot * pitch, row_src + c0, cw * 4u, w.bar);
+                mbar_wait(w.bar, w.parity);
+                w.parity ^= 1u;
             } else {
-#pragma unroll 8
-                for (uint32_t i = 0; i < quads; ++i) acc = acc4_exact2<METRIC>(acc, q4[i], r4[i]);
+                __syncwarp();
+                const uint32_t nvec = cw >> 2;             // 16-byte pieces per row
+                const uint32_t rpi = 32u / nvec;           // rows per warp instruction
+                const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
+                for (uint32_t t = 0; t < nr; t += rpi) {
+                    const uint32_t want = r0 + t + sub;      // rank of the row this lane moves
+                    const bool act = sub < rpi && t + sub < nr;
+                    const int src = act ? __fns(nm, 0, (int)want + 1) : 0;
+                    const uint32_t er = __shfl_sync(kFull, e, src);
+                    if (act)
+                        cp_async16(w.stage + (t + sub) * pitch + piece * 4,
+                                   g.vec + (size_t)er * g.ld + c0 + piece * 4);
+                }
+                cp_async_wait_all();
+                __syncwarp();
             }
-            for (uint32_t i = quads * 4; i < lim; ++i) {
-                const float qv = w.sq[c0 + i], rv = mine[i];
+            if (computes && c0 < g.d) {
+                const uint32_t lim = min(cw, g.d - c0);
+                const uint32_t quads = lim >> 2;
+                const float4* r4 = reinterpret_cast<const float4*>(srow);
+                const float4* q4 = reinterpret_cast<const float4*>(w.sq + c0);
                 if (FAST) {
-                    if (METRIC == 0) {
-                        const float df = qv - rv;
-                        acc = fmaf(df, df, acc);
-                    } else {
-                        acc = fmaf(qv, rv, acc);
-                    }
+#pragma unroll 8
+                    for (uint32_t i = 0; i < quads; ++i) acc2 = acc4_fast<METRIC>(acc2, q4[i], r4[i]);
                 } else {
-                    acc = acc_exact<METRIC>(acc, qv, rv);
+#pragma unroll 8
+                    for (uint32_t i = 0; i < quads; ++i) acc = acc4_exact2<METRIC>(acc, q4[i], r4[i]);
+                }
+                for (uint32_t i = quads * 4; i < lim; ++i) {
+                    const float qv = w.sq[c0 + i], rv = srow[i];
+                    if (FAST) {
+                        if (METRIC == 0) {
+                            const float df = qv - rv;
+                            acc = fmaf(df, df, acc);
+                        } else {
+                            acc = fmaf(qv, rv, acc);
+                        }
+                    } else {
+                        acc = acc_exact<METRIC>(acc, qv, rv);
+                    }
                 }
             }
         }
+        float dist;
+        if (FAST) dist = finish_exact<METRIC>(f2_lo(acc2) + f2_hi(acc2) + acc);
+        else dist = finish_exact<METRIC>(acc);
+        const float got = __shfl_sync(kFull, dist, (int)(slot & 31u));
+        if (mine_round) result = got;
     }
-    if (!need) return kInf;
-    if (FAST) return finish_exact<METRIC>(f2_lo(acc2) + f2_hi(acc2) + acc);
-    return finish_exact<METRIC>(acc);
+    return result;
 }
 
 }  // namespace tsdg_dev

@@ -132,7 +132,7 @@ void fill_bf_layout(BfArgs& a) {
     Carve c;
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
+    a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
     a.off_cid = c.take(a.m * kSegPitch * 4);
     a.off_cdist = c.take(a.m * kSegPitch * 4);
     a.off_csize = c.take(a.m * 4);
@@ -145,8 +145,10 @@ void fill_bf_layout(BfArgs& a) {
     a.warp_smem = round_up(c.total, 128);
 }
 
-// Tuning knobs (environment, read per launch): TSDG_STAGE=tma|ldgsts,
-// TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency).
+// Tuning knobs (environment, read per launch): TSDG_STAGE=tma (default)|ldgsts,
+// TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency; default 0),
+// TSDG_BF_WARPS=<warps per CTA> (default 1: finest shared-memory granularity),
+// TSDG_SLOTS=<staged rows per gather round> (default 32).
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoi(v) : dflt;
@@ -219,15 +221,17 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_stats = d_stats;
     a.work_counter = next_counter(idx, st);
     a.dch = staging_dims(idx->ld);
-    a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 3);
+    a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 32)));
+    a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
     fill_bf_layout(a);
-    const size_t smem = (size_t)a.warp_smem * kBfWarps;
-    const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST, env_is("TSDG_STAGE", "tma"),
-                                  a.k <= 31);
+    const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
+    const size_t smem = (size_t)a.warp_smem * wpc;
+    const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST,
+                                  !env_is("TSDG_STAGE", "ldgsts"), a.k <= 31);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute(bf)");
-    const int grid = grid_for(kern, kBfWarps * 32, smem, idx->sm_count, nq, kBfWarps);
-    kern<<<grid, kBfWarps * 32, smem, st>>>(a);
+    const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq, wpc);
+    kern<<<grid, wpc * 32, smem, st>>>(a);
     g_launches++;
     cuda_check(cudaGetLastError(), "bf_kernel launch");
 }
@@ -288,14 +292,15 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.walk_evals = wb.evals;
     a.work_counter = next_counter(idx, st);
     a.dch = staging_dims(idx->ld);
+    a.slots = 32;
     Carve c;
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_stage = c.take(32 * (a.dch + 4) * 4, 128);
+    a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
     a.warp_smem = round_up(c.total, 128);
     const size_t smem = (size_t)a.warp_smem * kGrWarps;
     using GrKernel = void (*)(GrArgs);
-    const bool tma = env_is("TSDG_STAGE", "tma");
+    const bool tma = !env_is("TSDG_STAGE", "ldgsts");
     GrKernel kern;
     if (idx->metric == 0)
         kern = fast ? (tma ? greedy_walk_kernel<0, true, kStageTma> : greedy_walk_kernel<0, true, kStageLdgsts>)

@@ -34,9 +34,14 @@ for k in ks:
     dd = torch.empty((nq, k), dtype=torch.float32, device=dev)
     cc = torch.empty(nq, dtype=torch.int32, device=dev)
     stt = torch.empty((nq, 4), dtype=torch.int32, device=dev)
-    for mode, stage, pf in variants:
+    for var in variants:
+        mode, stage, pf = var[:3]
+        wpc = var[3] if len(var) > 3 else "1"
+        slots = var[4] if len(var) > 4 else "32"
         os.environ["TSDG_STAGE"] = stage
         os.environ["TSDG_PREFETCH"] = pf
+        os.environ["TSDG_BF_WARPS"] = wpc
+        os.environ["TSDG_SLOTS"] = slots
         m = _native.MODE_FAST if mode == "fast" else _native.MODE_DETERMINISTIC
 
         def step():
@@ -61,7 +66,7 @@ for k in ks:
         rec = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(), ds.gt, 10)
         ms = float(np.median(times))
         alg = 4 * ds.base.shape[1] * st[:, 1].sum() + 4 * st[:, 3].sum() + nq * (4 * ds.base.shape[1] + 8 * k)
-        print(json.dumps({"k": k, "mode": mode, "stage": stage, "prefetch": pf, "ms": ms,
+        print(json.dumps({"k": k, "mode": mode, "stage": stage, "prefetch": pf, "warps": wpc, "slots": slots, "ms": ms,
                           "qps": nq / ms * 1e3, "recall10": rec, "alg_GBps": alg / ms / 1e6,
                           "evals_q": float(st[:, 1].mean()), "hops_q": float(st[:, 0].mean())}),
               flush=True)
