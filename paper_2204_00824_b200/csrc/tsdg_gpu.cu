@@ -148,7 +148,7 @@ void fill_bf_layout(BfArgs& a) {
 // Tuning knobs (environment, read per launch): TSDG_STAGE=tma (default)|ldgsts,
 // TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency; default 0),
 // TSDG_BF_WARPS=<warps per CTA> (default 1: finest shared-memory granularity),
-// TSDG_SLOTS=<staged rows per gather round> (default 32).
+// TSDG_SLOTS=<staged rows per gather round> (default 16).
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoi(v) : dflt;
@@ -221,7 +221,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_stats = d_stats;
     a.work_counter = next_counter(idx, st);
     a.dch = staging_dims(idx->ld);
-    a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 32)));
+    a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
     a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
     fill_bf_layout(a);
     const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
