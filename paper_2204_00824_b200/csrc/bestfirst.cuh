@@ -73,6 +73,11 @@ struct BfWarp {
     float* rdist;
 };
 
+// e % m without a hardware divide when m is a power of two (the usual 8 / 16)
+__device__ __forceinline__ uint32_t seg_of(uint32_t e, uint32_t m) {
+    return (m & (m - 1)) == 0 ? (e & (m - 1)) : e % m;
+}
+
 // ---- membership scans: each lane its own segment, 8 x LDS.128 ------------------
 __device__ __forceinline__ bool seg_scan(const uint32_t* base, uint32_t sz, uint32_t e) {
     const uint4* p = reinterpret_cast<const uint4*>(base);
@@ -90,17 +95,17 @@ __device__ __forceinline__ bool seg_scan(const uint32_t* base, uint32_t sz, uint
     return hit;
 }
 __device__ __forceinline__ bool v_contains(const BfWarp& w, uint32_t m, uint32_t e) {
-    const uint32_t s = e % m;
+    const uint32_t s = seg_of(e, m);
     return seg_scan(w.vid + s * kSegPitch, w.vsize[s], e);
 }
 __device__ __forceinline__ bool c_contains(const BfWarp& w, uint32_t m, uint32_t e) {
-    const uint32_t s = e % m;
+    const uint32_t s = seg_of(e, m);
     return seg_scan(w.cid + s * kSegPitch, w.csize[s], e);
 }
 
 // segmented.cpp:68-79 (warp-uniform call)
 __device__ __forceinline__ void v_add(BfWarp& w, uint32_t m, uint32_t u, int lane) {
-    const uint32_t s = u % m;
+    const uint32_t s = seg_of(u, m);
     uint32_t* seg = w.vid + s * kSegPitch;
     const uint32_t sz = w.vsize[s];
     const bool hit = lane < (int)sz && seg[lane] == u;
@@ -121,7 +126,7 @@ __device__ __forceinline__ void v_add(BfWarp& w, uint32_t m, uint32_t u, int lan
 // the newcomer itself was dropped).  Warp-uniform call.
 __device__ __forceinline__ uint32_t c_push(BfWarp& w, uint32_t m, uint32_t e, float dist,
                                            uint32_t& total, uint32_t& evictions, int lane) {
-    const uint32_t s = e % m;
+    const uint32_t s = seg_of(e, m);
     uint32_t* sid = w.cid + s * kSegPitch;
     float* sdist = w.cdist + s * kSegPitch;
     uint32_t sz = w.csize[s];
@@ -173,7 +178,7 @@ __device__ __forceinline__ void c_pop_min(BfWarp& w, uint32_t m, float& pd, uint
     warp_argmin(hd, hi);
     pd = hd;
     pu = hi;
-    const uint32_t s = hi % m;
+    const uint32_t s = seg_of(hi, m);
     uint32_t* sid = w.cid + s * kSegPitch;
     float* sdist = w.cdist + s * kSegPitch;
     const uint32_t sz = w.csize[s];

@@ -72,19 +72,19 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
     return r;
 }
 
-// Exact: acc continues the reference's sequential sum over 4 more dims.
+// Exact: acc continues the reference's sequential sum over 4 more dims.  Operands
+// arrive as packed f32 pairs straight from LDS.128 (ulonglong2), so the paired
+// FADD2/FMUL2 need no register shuffling.
 template <int METRIC>
-__device__ __forceinline__ float acc4_exact2(float acc, float4 q, float4 r) {
-    const unsigned long long q01 = f2_pack(q.x, q.y), q23 = f2_pack(q.z, q.w);
-    const unsigned long long r01 = f2_pack(r.x, r.y), r23 = f2_pack(r.z, r.w);
+__device__ __forceinline__ float acc4_exact2(float acc, ulonglong2 q, ulonglong2 r) {
     unsigned long long t01, t23;
     if (METRIC == 0) {
-        const unsigned long long d01 = f2_sub(q01, r01), d23 = f2_sub(q23, r23);
+        const unsigned long long d01 = f2_sub(q.x, r.x), d23 = f2_sub(q.y, r.y);
         t01 = f2_mul(d01, d01);
         t23 = f2_mul(d23, d23);
     } else {
-        t01 = f2_mul(q01, r01);
-        t23 = f2_mul(q23, r23);
+        t01 = f2_mul(q.x, r.x);
+        t23 = f2_mul(q.y, r.y);
     }
     acc = __fadd_rn(acc, f2_lo(t01));
     acc = __fadd_rn(acc, f2_hi(t01));
@@ -93,20 +93,46 @@ __device__ __forceinline__ float acc4_exact2(float acc, float4 q, float4 r) {
     return acc;
 }
 
-// Fast: two packed accumulators (even/odd lanes of the pair).
+// Fast: two packed accumulators (even/odd dims).
 template <int METRIC>
-__device__ __forceinline__ unsigned long long acc4_fast(unsigned long long acc, float4 q, float4 r) {
-    const unsigned long long q01 = f2_pack(q.x, q.y), q23 = f2_pack(q.z, q.w);
-    const unsigned long long r01 = f2_pack(r.x, r.y), r23 = f2_pack(r.z, r.w);
+__device__ __forceinline__ unsigned long long acc4_fast(unsigned long long acc, ulonglong2 q,
+                                                        ulonglong2 r) {
     if (METRIC == 0) {
-        const unsigned long long d01 = f2_sub(q01, r01), d23 = f2_sub(q23, r23);
+        const unsigned long long d01 = f2_sub(q.x, r.x), d23 = f2_sub(q.y, r.y);
         acc = f2_fma(d01, d01, acc);
         acc = f2_fma(d23, d23, acc);
     } else {
-        acc = f2_fma(q01, r01, acc);
-        acc = f2_fma(q23, r23, acc);
+        acc = f2_fma(q.x, r.x, acc);
+        acc = f2_fma(q.y, r.y, acc);
     }
     return acc;
+}
+
+// Sum over quads [q0, q1) of one staged row; full unroll for the d = 128 case.
+template <int METRIC, bool FAST>
+__device__ __forceinline__ void row_quads(const float* srow, const float* sq, uint32_t q0,
+                                          uint32_t q1, float& acc, unsigned long long& acc2) {
+    const ulonglong2* r2 = reinterpret_cast<const ulonglong2*>(srow);
+    const ulonglong2* q2 = reinterpret_cast<const ulonglong2*>(sq);
+    if (q0 == 0 && q1 == 32) {
+#pragma unroll
+        for (uint32_t i = 0; i < 32; ++i) {
+            if (FAST) acc2 = acc4_fast<METRIC>(acc2, q2[i], r2[i]);
+            else acc = acc4_exact2<METRIC>(acc, q2[i], r2[i]);
+        }
+    } else if (q1 - q0 == 16) {
+#pragma unroll
+        for (uint32_t i = 0; i < 16; ++i) {
+            if (FAST) acc2 = acc4_fast<METRIC>(acc2, q2[q0 + i], r2[q0 + i]);
+            else acc = acc4_exact2<METRIC>(acc, q2[q0 + i], r2[q0 + i]);
+        }
+    } else {
+#pragma unroll 4
+        for (uint32_t i = q0; i < q1; ++i) {
+            if (FAST) acc2 = acc4_fast<METRIC>(acc2, q2[i], r2[i]);
+            else acc = acc4_exact2<METRIC>(acc, q2[i], r2[i]);
+        }
+    }
 }
 
 // Stage the rows of the lanes in `need` (row id e per lane) and return each such
@@ -129,8 +155,12 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
         const uint32_t nr = min(g.slots, cnt - r0);
         const bool mine_round = need && rank >= r0 && rank < r0 + nr;
         const uint32_t slot = rank - r0;
-        const bool computes = (uint32_t)lane < nr;
-        const float* srow = w.stage + lane * pitch;  // slot computed by this lane
+        // fast mode with <= 16 slots: lanes l and l+16 reduce the two halves of slot l
+        const bool split = FAST && g.slots <= 16;
+        const uint32_t cslot = split ? ((uint32_t)lane & 15u) : (uint32_t)lane;
+        const bool half = split && lane >= 16;
+        const bool computes = cslot < nr;
+        const float* srow = w.stage + cslot * pitch;  // slot reduced by this lane
         float acc = 0.0f;
         unsigned long long acc2 = 0ull;
         for (uint32_t c0 = 0; c0 < g.ld; c0 += g.dch) {
@@ -163,33 +193,39 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
             if (computes && c0 < g.d) {
                 const uint32_t lim = min(cw, g.d - c0);
                 const uint32_t quads = lim >> 2;
-                const float4* r4 = reinterpret_cast<const float4*>(srow);
-                const float4* q4 = reinterpret_cast<const float4*>(w.sq + c0);
-                if (FAST) {
-#pragma unroll 8
-                    for (uint32_t i = 0; i < quads; ++i) acc2 = acc4_fast<METRIC>(acc2, q4[i], r4[i]);
-                } else {
-#pragma unroll 8
-                    for (uint32_t i = 0; i < quads; ++i) acc = acc4_exact2<METRIC>(acc, q4[i], r4[i]);
+                // fast mode: two lanes per slot when slots <= 16 (halves of the row)
+                uint32_t qa = 0, qb = quads;
+                if (FAST && split) {
+                    const uint32_t h = quads >> 1;
+                    qa = half ? h : 0;
+                    qb = half ? quads : h;
                 }
-                for (uint32_t i = quads * 4; i < lim; ++i) {
-                    const float qv = w.sq[c0 + i], rv = srow[i];
-                    if (FAST) {
-                        if (METRIC == 0) {
-                            const float df = qv - rv;
-                            acc = fmaf(df, df, acc);
+                row_quads<METRIC, FAST>(srow, w.sq + c0, qa, qb, acc, acc2);
+                if (!(FAST && split && half)) {
+                    for (uint32_t i = quads * 4; i < lim; ++i) {
+                        const float qv = w.sq[c0 + i], rv = srow[i];
+                        if (FAST) {
+                            if (METRIC == 0) {
+                                const float df = qv - rv;
+                                acc = fmaf(df, df, acc);
+                            } else {
+                                acc = fmaf(qv, rv, acc);
+                            }
                         } else {
-                            acc = fmaf(qv, rv, acc);
+                            acc = acc_exact<METRIC>(acc, qv, rv);
                         }
-                    } else {
-                        acc = acc_exact<METRIC>(acc, qv, rv);
                     }
                 }
             }
         }
         float dist;
-        if (FAST) dist = finish_exact<METRIC>(f2_lo(acc2) + f2_hi(acc2) + acc);
-        else dist = finish_exact<METRIC>(acc);
+        if (FAST) {
+            float part = f2_lo(acc2) + f2_hi(acc2) + acc;
+            if (split) part += __shfl_xor_sync(kFull, part, 16);
+            dist = finish_exact<METRIC>(part);
+        } else {
+            dist = finish_exact<METRIC>(acc);
+        }
         const float got = __shfl_sync(kFull, dist, (int)(slot & 31u));
         if (mine_round) result = got;
     }

@@ -298,7 +298,8 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.off_query = c.take(a.ld * 4);
     a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
     a.warp_smem = round_up(c.total, 128);
-    const size_t smem = (size_t)a.warp_smem * kGrWarps;
+    const int wpc = std::max(1, std::min(kGrWarps, env_int("TSDG_GR_WARPS", 1)));
+    const size_t smem = (size_t)a.warp_smem * wpc;
     using GrKernel = void (*)(GrArgs);
     const bool tma = !env_is("TSDG_STAGE", "ldgsts");
     GrKernel kern;
@@ -311,8 +312,8 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
         kern = fast ? greedy_walk_kernel<2, true, kStageLdgsts> : greedy_walk_kernel<2, false, kStageLdgsts>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute(greedy)");
-    const int grid = grid_for(kern, kGrWarps * 32, smem, idx->sm_count, nq * t0, kGrWarps);
-    kern<<<grid, kGrWarps * 32, smem, st>>>(a);
+    const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq * t0, wpc);
+    kern<<<grid, wpc * 32, smem, st>>>(a);
     g_launches++;
     cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
 }
