@@ -86,7 +86,11 @@ struct tsdg_gpu_index {
     uint32_t counter_slot = 0;
     std::map<uint32_t, uint32_t*> degcut;
     std::mutex mu;
-    cudaStream_t stream = nullptr;  // for the host-pointer entry points
+    cudaStream_t stream = nullptr;   // for the host-pointer entry points
+    cudaStream_t stream2 = nullptr;  // second pipeline stream (copy/compute overlap)
+    // grow-only device scratch for the host-pointer entry points
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
 };
 
 namespace {
@@ -109,6 +113,8 @@ const uint32_t* get_degcut(tsdg_gpu_index* idx, uint32_t cut, cudaStream_t st) {
                                                              idx->n, cut, out);
         g_launches++;
         cuda_check(cudaGetLastError(), "deg_cut_kernel");
+        // the table is shared by later launches on any stream
+        cuda_check(cudaStreamSynchronize(st), "deg_cut_kernel");
     }
     idx->degcut[cut] = out;
     return out;
@@ -400,6 +406,13 @@ int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint6
         for (uint64_t j = 0; j < E; ++j)
             if (targets[j] >= n) fail(TSDG_EINVAL, "index_create: edge target out of range");
         cuda_check(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithFlags(&idx->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+        // keep stream-ordered allocations cached across calls (no re-mapping per search)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
         // vectors, rows padded to ld floats (16-byte aligned for TMA bulk copies)
         const size_t nv = (size_t)std::max<uint32_t>(n, 1) * idx->ld;
         cuda_check(cudaMalloc(&idx->vec, nv * sizeof(float)), "cudaMalloc(vectors)");
@@ -462,13 +475,16 @@ int tsdg_gpu_index_destroy(tsdg_gpu_index* idx) {
         if (!idx) return;
         DeviceGuard dg(idx->device);
         cudaStreamSynchronize(idx->stream);
+        cudaStreamSynchronize(idx->stream2);
         for (auto& kv : idx->degcut) cudaFree(kv.second);
+        if (idx->scratch) cudaFree(idx->scratch);
         cudaFree(idx->vec);
         cudaFree(idx->adj);
         cudaFree(idx->lam);
         cudaFree(idx->deg_full);
         cudaFree(idx->counters);
         cudaStreamDestroy(idx->stream);
+        cudaStreamDestroy(idx->stream2);
         delete idx;
     });
 }
@@ -533,33 +549,63 @@ int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_
         if (nq == 0) return;
         std::lock_guard<std::mutex> lk(idx->mu);
         DeviceGuard dg(idx->device);
-        cudaStream_t st = idx->stream;
         const uint32_t k = params->k;
-        float* dq = dev_alloc<float>((size_t)nq * idx->d, st);
-        uint32_t* di = dev_alloc<uint32_t>((size_t)nq * k, st);
-        float* dd = dev_alloc<float>((size_t)nq * k, st);
-        uint32_t* dc = dev_alloc<uint32_t>(nq, st);
-        tsdg_query_stats* ds = stats ? dev_alloc<tsdg_query_stats>(nq, st) : nullptr;
-        cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st),
-                   "cudaMemcpyAsync(queries)");
-        launch_bestfirst(idx, dq, nq, query_index_base, params, mode, di, dd, dc, ds, st);
-        cuda_check(cudaMemcpyAsync(ids, di, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
-        if (dists)
-            cuda_check(cudaMemcpyAsync(dists, dd, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st),
-                       "D2H dists");
-        if (counts)
-            cuda_check(cudaMemcpyAsync(counts, dc, (size_t)nq * 4, cudaMemcpyDeviceToHost, st),
-                       "D2H counts");
-        if (stats)
-            cuda_check(cudaMemcpyAsync(stats, ds, (size_t)nq * sizeof(tsdg_query_stats),
+        // grow-only scratch: queries | ids | dists | counts | stats
+        const size_t bq = (size_t)nq * idx->d * 4, bi = (size_t)nq * k * 4, bc = (size_t)nq * 4,
+                     bs = (size_t)nq * sizeof(tsdg_query_stats);
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t need = al(bq) + 2 * al(bi) + al(bc) + al(bs);
+        if (need > idx->scratch_bytes) {
+            cuda_check(cudaStreamSynchronize(idx->stream), "sync");
+            cuda_check(cudaStreamSynchronize(idx->stream2), "sync");
+            if (idx->scratch) cudaFree(idx->scratch);
+            idx->scratch = nullptr;
+            idx->scratch_bytes = 0;
+            cuda_check(cudaMalloc(&idx->scratch, need), "cudaMalloc(scratch)");
+            idx->scratch_bytes = need;
+        }
+        char* base = static_cast<char*>(idx->scratch);
+        float* dq = reinterpret_cast<float*>(base);
+        uint32_t* di = reinterpret_cast<uint32_t*>(base + al(bq));
+        float* dd = reinterpret_cast<float*>(base + al(bq) + al(bi));
+        uint32_t* dc = reinterpret_cast<uint32_t*>(base + al(bq) + 2 * al(bi));
+        tsdg_query_stats* ds =
+            reinterpret_cast<tsdg_query_stats*>(base + al(bq) + 2 * al(bi) + al(bc));
+        // Copy/compute pipeline: the batch is cut into chunks alternating between two
+        // streams, so chunk c+1's upload overlaps chunk c's search and chunk c-1's
+        // download.  Each chunk keeps its global query index (RNG stream fork(base+q)).
+        get_degcut(idx, params->lambda_cut, idx->stream);
+        const uint32_t nchunks = nq >= 4096 ? 4 : 1;
+        const uint32_t csz = (nq + nchunks - 1) / nchunks;
+        for (uint32_t c = 0; c < nchunks; ++c) {
+            const uint32_t q0 = c * csz;
+            if (q0 >= nq) break;
+            const uint32_t cn = std::min(csz, nq - q0);
+            cudaStream_t st = (c & 1) ? idx->stream2 : idx->stream;
+            cuda_check(cudaMemcpyAsync(dq + (size_t)q0 * idx->d, queries + (size_t)q0 * idx->d,
+                                       (size_t)cn * idx->d * 4, cudaMemcpyHostToDevice, st),
+                       "cudaMemcpyAsync(queries)");
+            launch_bestfirst(idx, dq + (size_t)q0 * idx->d, cn, query_index_base + q0, params, mode,
+                             di + (size_t)q0 * k, dd + (size_t)q0 * k, dc + q0,
+                             stats ? ds + q0 : nullptr, st);
+            cuda_check(cudaMemcpyAsync(ids + (size_t)q0 * k, di + (size_t)q0 * k, (size_t)cn * k * 4,
                                        cudaMemcpyDeviceToHost, st),
-                       "D2H stats");
-        cudaFreeAsync(dq, st);
-        cudaFreeAsync(di, st);
-        cudaFreeAsync(dd, st);
-        cudaFreeAsync(dc, st);
-        if (ds) cudaFreeAsync(ds, st);
-        cuda_check(cudaStreamSynchronize(st), "bestfirst_search");
+                       "D2H ids");
+            if (dists)
+                cuda_check(cudaMemcpyAsync(dists + (size_t)q0 * k, dd + (size_t)q0 * k,
+                                           (size_t)cn * k * 4, cudaMemcpyDeviceToHost, st),
+                           "D2H dists");
+            if (counts)
+                cuda_check(cudaMemcpyAsync(counts + q0, dc + q0, (size_t)cn * 4,
+                                           cudaMemcpyDeviceToHost, st),
+                           "D2H counts");
+            if (stats)
+                cuda_check(cudaMemcpyAsync(stats + q0, ds + q0, (size_t)cn * sizeof(tsdg_query_stats),
+                                           cudaMemcpyDeviceToHost, st),
+                           "D2H stats");
+        }
+        cuda_check(cudaStreamSynchronize(idx->stream), "bestfirst_search");
+        cuda_check(cudaStreamSynchronize(idx->stream2), "bestfirst_search");
     });
 }
 
