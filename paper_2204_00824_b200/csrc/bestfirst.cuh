@@ -55,7 +55,8 @@ struct BfArgs {
     uint32_t* work_counter;
     uint32_t dch;           // staged dims per row per round (multiple of 8, <= 128)
     uint32_t slots;         // staged rows per gather round (1..32)
-    uint32_t prefetch;      // bit 0: next-chunk rows, bit 1: admitted adjacency
+    uint32_t prefetch;      // bit 0: next-chunk rows (L2), bit 1: admitted adjacency (L2),
+                            // bit 2: speculative next-hop adjacency load (registers)
     // per-warp shared-memory carve (bytes)
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
         off_vsize, off_voldest, off_rid, off_rdist, off_bar;
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
     const float kInf = __int_as_float(0x7f800000);
     const bool pf_rows = (a.prefetch & 1u) != 0;
     const bool pf_adj = (a.prefetch & 2u) != 0;
+    const bool spec = (a.prefetch & 4u) != 0;
 
     for (;;) {
         uint32_t q = 0;
@@ -323,6 +325,8 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
         else r_push_smem(w, rn, si, sd, lane);
         c_push(w, a.m, si, sd, ctotal, evictions, lane);
         float rfar = KREG ? __shfl_sync(kFull, rr.d, rn - 1) : w.rdist[rn - 1];
+        // speculative next expansion (see below): its deg + first 64 adjacency entries
+        uint32_t spec_u = kInvalid, spec_deg = 0, spec_e0 = kInvalid, spec_e1 = kInvalid;
 
         while (ctotal > 0 && hops < a.hop_limit) {  // :73
             ++hops;
@@ -330,11 +334,20 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
             uint32_t u;
             c_pop_min(w, a.m, pd, u, ctotal, lane);
             if (pd > __fadd_rn(rfar, a.delta)) break;  // :79
-            // issue the dependent loads first, then V.add while they fly
+            // issue the dependent loads first (unless the speculation already did), then
+            // V.add while they fly
             const uint32_t* arow = a.adj + (size_t)u * a.R;
-            const uint32_t deg = __ldg(a.degcut + u);
-            uint32_t e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
-            uint32_t e_next2 = (uint32_t)lane + 32 < a.R ? __ldg(arow + 32 + lane) : kInvalid;
+            uint32_t deg, e_next, e_next2;
+            if (u == spec_u) {
+                deg = spec_deg;
+                e_next = spec_e0;
+                e_next2 = spec_e1;
+            } else {
+                deg = __ldg(a.degcut + u);
+                e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
+                e_next2 = (uint32_t)lane + 32 < a.R ? __ldg(arow + 32 + lane) : kInvalid;
+            }
+            spec_u = kInvalid;
             v_add(w, a.m, u, lane);
             examined += deg;
             for (uint32_t base = 0; base < deg; base += 32) {
@@ -354,6 +367,33 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
                     prefetch_rows(a, nv, e_next);
                 }
                 float dist = gather_eval<METRIC, FAST, STAGE>(w.st, g, need, e, lane);
+                if (spec && base + 32 >= deg) {
+                    // Last chunk of the hop: the next pop is C's minimum after these
+                    // admissions = closer of (current C head, best candidate passing the
+                    // admission test) in all but rare eviction / tie cases.  Issue its
+                    // deg_cut + adjacency loads now so they overlap the admission replay;
+                    // the next hop uses them only if it pops exactly that node.
+                    float cd = (need && (dist < rfar || rn < a.k)) ? dist : kInf;
+                    uint32_t ci = (need && (dist < rfar || rn < a.k)) ? e : kInvalid;
+                    for (uint32_t sg = lane; sg < a.m; sg += 32) {
+                        if (w.csize[sg] != 0) {
+                            const float hd = w.cdist[sg * kSegPitch];
+                            const uint32_t hi = w.cid[sg * kSegPitch];
+                            if (closer(hd, hi, cd, ci)) {
+                                cd = hd;
+                                ci = hi;
+                            }
+                        }
+                    }
+                    warp_argmin(cd, ci);
+                    spec_u = ci;
+                    if (ci != kInvalid) {
+                        const uint32_t* srow = a.adj + (size_t)ci * a.R;
+                        spec_deg = __ldg(a.degcut + ci);
+                        spec_e0 = (uint32_t)lane < a.R ? __ldg(srow + lane) : kInvalid;
+                        spec_e1 = (uint32_t)lane + 32 < a.R ? __ldg(srow + 32 + lane) : kInvalid;
+                    }
+                }
                 unsigned pending = __ballot_sync(kFull, need);
                 unsigned revivable = __ballot_sync(kFull, inC);
                 evals += __popc(pending);
