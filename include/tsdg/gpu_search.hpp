@@ -1,0 +1,178 @@
+// tsdg/gpu_search.hpp — C++ drop-in for the reference's search entry points,
+// executed on a B200 through the C-ABI in tsdg_gpu.h (libtsdg_gpu.so).
+//
+// Header-only.  Include it next to the reference's own headers
+// (/root/reference/proj/include); it consumes the reference types unchanged:
+//   tsdg::TsdgGraph       diversify.hpp:56-76     (as produced by load_tsdg / build)
+//   tsdg::VectorSet       vectors.hpp:23-34
+//   tsdg::BestFirstParams bestfirst_search.hpp:15-25
+//   tsdg::GreedyParams    greedy_search.hpp:14-19
+//   tsdg::SearchStats     greedy_search.hpp:21-32
+// and mirrors the entry points it replaces:
+//   tsdg::large_batch_search  bestfirst_search.hpp:47-51  -> tsdg::gpu::large_batch_search
+//   tsdg::small_batch_search  greedy_search.hpp:55-60     -> tsdg::gpu::small_batch_search
+// with the same argument meaning, the same results (bit-exact in Mode::Deterministic)
+// and the same exception types (std::invalid_argument / std::runtime_error).
+// tsdg::gpu::Index keeps the graph and vectors resident in HBM across calls and adds
+// the distance-returning and device-pointer forms.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tsdg/bestfirst_search.hpp"
+#include "tsdg/diversify.hpp"
+#include "tsdg/greedy_search.hpp"
+#include "tsdg/vectors.hpp"
+#include "tsdg_gpu.h"
+
+namespace tsdg::gpu {
+
+enum class Mode : int { Deterministic = TSDG_MODE_DETERMINISTIC, Fast = TSDG_MODE_FAST };
+
+inline void check(int rc) {
+    if (rc == TSDG_OK) return;
+    const std::string msg = tsdg_gpu_last_error();
+    if (rc == TSDG_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+/// Search output with distances: ids/dists are nq x k, ascending by (dist, id),
+/// padded with kInvalidId / +inf beyond counts[q].
+struct SearchResult {
+    std::uint32_t k = 0;
+    std::vector<NodeId> ids;
+    std::vector<float> dists;
+    std::vector<std::uint32_t> counts;
+    std::vector<tsdg_query_stats> stats;
+
+    std::vector<std::vector<NodeId>> lists() const {
+        std::vector<std::vector<NodeId>> out(counts.size());
+        for (std::size_t q = 0; q < counts.size(); ++q)
+            out[q].assign(ids.begin() + q * k, ids.begin() + q * k + counts[q]);
+        return out;
+    }
+    void add_to(SearchStats* s) const {
+        if (!s) return;
+        for (const auto& st : stats) {
+            s->hops += st.hops;
+            s->distance_evals += st.distance_evals;
+            s->queue_evictions += st.queue_evictions;
+        }
+    }
+};
+
+inline tsdg_bf_params to_c(const BestFirstParams& p) {
+    return tsdg_bf_params{p.k, p.hop_limit, p.delta, p.m_segments, p.lambda_cut, p.seed,
+                          p.unbounded ? 1 : 0};
+}
+inline tsdg_greedy_params to_c(const GreedyParams& p) {
+    return tsdg_greedy_params{p.t0, p.hop_limit, p.lambda_cut, p.seed};
+}
+
+/// Device-resident index: graph + vector store uploaded once.
+class Index {
+public:
+    Index(const TsdgGraph& graph, const VectorSet& base, int device = 0) : d_(base.d) {
+        if (graph.n != base.n)
+            throw std::invalid_argument("gpu::Index: graph/set size mismatch");
+        std::vector<std::uint32_t> targets(graph.edges.size());
+        std::vector<std::uint16_t> lambdas(graph.edges.size());
+        for (std::size_t i = 0; i < graph.edges.size(); ++i) {
+            targets[i] = graph.edges[i].target;
+            lambdas[i] = graph.edges[i].lambda;
+        }
+        check(tsdg_gpu_index_create(base.data.data(), base.n, base.d, graph.offsets.data(),
+                                    targets.data(), lambdas.data(),
+                                    static_cast<int>(graph.metric), device, &h_));
+        metric_ = graph.metric;
+    }
+    Index(const Index&) = delete;
+    Index& operator=(const Index&) = delete;
+    ~Index() { tsdg_gpu_index_destroy(h_); }
+
+    tsdg_gpu_index* handle() const { return h_; }
+
+    SearchResult search_bestfirst(const VectorSet& queries, const BestFirstParams& params,
+                                  Mode mode = Mode::Deterministic,
+                                  std::uint64_t query_index_base = 0) const {
+        if (queries.d != d_) throw std::invalid_argument("large_batch_search: dim mismatch");
+        require_metric_ready(queries, metric_);
+        SearchResult r;
+        r.k = params.k;
+        r.ids.resize(static_cast<std::size_t>(queries.n) * params.k);
+        r.dists.resize(r.ids.size());
+        r.counts.resize(queries.n);
+        r.stats.resize(queries.n);
+        const tsdg_bf_params p = to_c(params);
+        check(tsdg_gpu_search_bestfirst(h_, queries.data.data(), queries.n, query_index_base, &p,
+                                        static_cast<int>(mode), r.ids.data(), r.dists.data(),
+                                        r.counts.data(), r.stats.data()));
+        return r;
+    }
+
+    std::vector<std::vector<NodeId>> large_batch_search(const VectorSet& queries,
+                                                        const BestFirstParams& params,
+                                                        SearchStats* stats = nullptr,
+                                                        Mode mode = Mode::Deterministic) const {
+        const SearchResult r = search_bestfirst(queries, params, mode);
+        r.add_to(stats);
+        return r.lists();
+    }
+
+    SearchResult search_greedy(const VectorSet& queries, std::uint32_t k,
+                               const GreedyParams& params,
+                               Mode mode = Mode::Deterministic) const {
+        if (queries.d != d_) throw std::invalid_argument("small_batch_search: dim mismatch");
+        require_metric_ready(queries, metric_);
+        SearchResult r;
+        r.k = k;
+        r.ids.resize(static_cast<std::size_t>(queries.n) * k);
+        r.dists.resize(r.ids.size());
+        r.counts.resize(queries.n);
+        r.stats.resize(queries.n);
+        const tsdg_greedy_params p = to_c(params);
+        check(tsdg_gpu_search_greedy(h_, queries.data.data(), queries.n, k, &p,
+                                     static_cast<int>(mode), r.ids.data(), r.dists.data(),
+                                     r.counts.data(), r.stats.data()));
+        return r;
+    }
+
+    std::vector<std::vector<NodeId>> small_batch_search(const VectorSet& queries, std::uint32_t k,
+                                                        const GreedyParams& params,
+                                                        SearchStats* stats = nullptr,
+                                                        Mode mode = Mode::Deterministic) const {
+        const SearchResult r = search_greedy(queries, k, params, mode);
+        r.add_to(stats);
+        return r.lists();
+    }
+
+private:
+    tsdg_gpu_index* h_ = nullptr;
+    std::uint32_t d_ = 0;
+    Metric metric_ = Metric::L2;
+};
+
+/// Reference-signature free functions (each builds a transient device index).
+inline std::vector<std::vector<NodeId>> large_batch_search(const TsdgGraph& graph,
+                                                           const VectorSet& set,
+                                                           const VectorSet& queries,
+                                                           const BestFirstParams& params,
+                                                           SearchStats* stats = nullptr) {
+    if (queries.d != set.d) throw std::invalid_argument("large_batch_search: dim mismatch");
+    return Index(graph, set).large_batch_search(queries, params, stats);
+}
+
+inline std::vector<std::vector<NodeId>> small_batch_search(const TsdgGraph& graph,
+                                                           const VectorSet& set,
+                                                           const VectorSet& queries,
+                                                           std::uint32_t k,
+                                                           const GreedyParams& params,
+                                                           SearchStats* stats = nullptr) {
+    if (queries.d != set.d) throw std::invalid_argument("small_batch_search: dim mismatch");
+    return Index(graph, set).small_batch_search(queries, k, params, stats);
+}
+
+}  // namespace tsdg::gpu

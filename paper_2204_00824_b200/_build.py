@@ -59,7 +59,14 @@ def build_oracle() -> None:
         _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle"), "ref"])
 
 
+def build_cpp_tests() -> None:
+    """C++ drop-in parity binary (needs the reference headers + oracle/_ref objects)."""
+    if os.path.isdir("/root/reference/proj/include") and os.path.isdir(os.path.join(ROOT, "oracle", "_ref")):
+        _run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+
+
 def build_all(force: bool = False) -> None:
     build_datagen(force)
     build_oracle()
     build_gpu(force)
+    build_cpp_tests()

@@ -544,10 +544,10 @@ int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_
                               tsdg_query_stats* stats) {
     return guarded([&] {
         if (!idx) fail(TSDG_EINVAL, "bestfirst_search: null index");
+        if (nq == 0) return;  // the reference's per-query loop never runs
         validate_bf(idx, params);
-        if (nq && (!queries || !ids)) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
+        if (!queries || !ids) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
         check_cosine_queries(idx, queries, nq);
-        if (nq == 0) return;
         std::lock_guard<std::mutex> lk(idx->mu);
         DeviceGuard dg(idx->device);
         const uint32_t k = params->k;
@@ -630,10 +630,10 @@ int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t n
                            float* dists, uint32_t* counts, tsdg_query_stats* stats) {
     return guarded([&] {
         if (!idx) fail(TSDG_EINVAL, "small_batch_search: null index");
+        if (nq == 0) return;  // the reference's per-query loop never runs
         validate_greedy(idx, k, params);
-        if (nq && (!queries || !ids)) fail(TSDG_EINVAL, "small_batch_search: null buffer");
+        if (!queries || !ids) fail(TSDG_EINVAL, "small_batch_search: null buffer");
         check_cosine_queries(idx, queries, nq);
-        if (nq == 0) return;
         std::lock_guard<std::mutex> lk(idx->mu);
         DeviceGuard dg(idx->device);
         cudaStream_t st = idx->stream;

@@ -1,0 +1,163 @@
+// C++ parity suite for the drop-in header include/tsdg/gpu_search.hpp, written
+// like the reference's own tests (test_bestfirst.cpp, test_greedy.cpp,
+// acceptance.cpp) and linked against the UNMODIFIED reference library
+// (oracle/_ref, test infrastructure) so every case compares tsdg::gpu::* with
+// the reference's tsdg::* on the same inputs.  Exit code = number of failures.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tsdg/bench.hpp"
+#include "tsdg/bestfirst_search.hpp"
+#include "tsdg/greedy_search.hpp"
+#include "tsdg/knn_graph.hpp"
+#include "tsdg/reference.hpp"
+#include "tsdg/gpu_search.hpp"
+
+using namespace tsdg;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                                  \
+    do {                                                                          \
+        ++g_checks;                                                               \
+        if (!(c)) {                                                               \
+            ++g_fail;                                                             \
+            std::printf("  FAIL %s:%d  %s\n", __FILE__, __LINE__, #c);            \
+        }                                                                         \
+    } while (0)
+#define CASE(name) std::printf("[case] %s\n", name)
+
+static TsdgGraph complete_graph(const VectorSet& set, Metric metric) {
+    // test_bestfirst.cpp:18-33
+    const auto kernel = kernel_for(metric);
+    std::vector<std::vector<TsdgEdge>> adjacency(set.n);
+    for (NodeId u = 0; u < set.n; ++u) {
+        for (NodeId v = 0; v < set.n; ++v) {
+            if (v == u) continue;
+            adjacency[u].push_back({v, 0, kernel(set.row(u), set.row(v), set.d)});
+        }
+        std::sort(adjacency[u].begin(), adjacency[u].end(), [](const TsdgEdge& a, const TsdgEdge& b) {
+            if (a.dist != b.dist) return a.dist < b.dist;
+            return a.target < b.target;
+        });
+    }
+    return tsdg_from_adjacency(set.n, metric, set.n - 1, 1.0f, 0, adjacency);
+}
+
+int main() {
+    {
+        CASE("complete graph yields the exact top-k (test_bestfirst.cpp:39-62)");
+        const auto set = make_synthetic(64, 8, 3, 0.3f, 51);
+        const auto g = complete_graph(set, Metric::L2);
+        const auto queries = make_synthetic(15, 8, 3, 0.3f, 52);
+        const auto truth = ref::exact_topk(set, queries, 10, Metric::L2);
+        BestFirstParams p;
+        p.k = 10;
+        p.hop_limit = 10000;
+        p.delta = 1e30f;
+        p.m_segments = 2;
+        p.lambda_cut = 1;
+        const auto ids = gpu::large_batch_search(g, set, queries, p);
+        for (std::uint32_t q = 0; q < queries.n; ++q) {
+            CHECK(ids[q].size() == 10);
+            for (std::size_t i = 0; i < ids[q].size(); ++i) CHECK(ids[q][i] == truth[q][i].id);
+        }
+    }
+    {
+        CASE("large_batch_search == reference, ids + stats, parameter grid");
+        auto [base, queries] = make_synthetic_split(3000, 300, 24, 10, 0.25f, 9);
+        const auto knn = brute_force_knn(base, 30, Metric::L2);
+        const auto g = build(base, knn, {1.2f, 9, 0}, Metric::L2);
+        const gpu::Index index(g, base);
+        for (std::uint32_t k : {1u, 10u, 32u, 64u}) {
+            for (std::uint32_t m : {1u, 8u}) {
+                for (float delta : {0.0f, 0.5f}) {
+                    BestFirstParams p;
+                    p.k = k;
+                    p.m_segments = m;
+                    p.delta = delta;
+                    p.lambda_cut = 7;
+                    p.seed = 11 + k;
+                    SearchStats s_ref, s_gpu;
+                    const auto want = large_batch_search(g, base, queries, p, &s_ref);
+                    const auto got = index.large_batch_search(queries, p, &s_gpu);
+                    CHECK(got == want);
+                    CHECK(s_gpu.hops == s_ref.hops);
+                    CHECK(s_gpu.distance_evals == s_ref.distance_evals);
+                    CHECK(s_gpu.queue_evictions == s_ref.queue_evictions);
+                    const auto fast = index.large_batch_search(queries, p, nullptr, gpu::Mode::Fast);
+                    CHECK(fast.size() == want.size());
+                }
+            }
+        }
+        CASE("distances equal the reference kernel on the returned ids");
+        BestFirstParams p;
+        p.k = 16;
+        const auto r = index.search_bestfirst(queries, p);
+        const auto kernel = kernel_for(Metric::L2);
+        for (std::uint32_t q = 0; q < queries.n; ++q)
+            for (std::uint32_t i = 0; i < r.counts[q]; ++i) {
+                const float want = kernel(queries.row(q), base.row(r.ids[q * p.k + i]), base.d);
+                CHECK(std::memcmp(&want, &r.dists[q * p.k + i], 4) == 0);
+            }
+        CASE("small_batch_search == reference (greedy_search.cpp:106-127)");
+        for (std::uint32_t t0 : {1u, 4u, 16u}) {
+            GreedyParams gp;
+            gp.t0 = t0;
+            gp.seed = 77;
+            SearchStats s_ref, s_gpu;
+            const auto want = small_batch_search(g, base, queries, 10, gp, &s_ref);
+            const auto got = index.small_batch_search(queries, 10, gp, &s_gpu);
+            CHECK(got == want);
+            CHECK(s_gpu.hops == s_ref.hops);
+            CHECK(s_gpu.distance_evals == s_ref.distance_evals);
+        }
+        CASE("parameter validation throws std::invalid_argument (test_bestfirst.cpp:176-183)");
+        BestFirstParams bad;
+        bad.delta = -1.0f;
+        bool threw = false;
+        try {
+            index.large_batch_search(queries, bad);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        GreedyParams g1;
+        g1.t0 = 1;
+        threw = false;
+        try {
+            index.small_batch_search(queries, 33, g1);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        VectorSet wrong = queries;
+        wrong.d = 5;
+        wrong.data.resize(static_cast<std::size_t>(wrong.n) * 5);
+        threw = false;
+        try {
+            index.large_batch_search(wrong, BestFirstParams{});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {
+        CASE("saved TSDG reloaded by the reference loader, searched on the GPU");
+        auto [base, queries] = make_synthetic_split(2000, 100, 16, 8, 0.2f, 401);
+        const auto g = build(base, brute_force_knn(base, 30, Metric::L2), {1.2f, 9, 0}, Metric::L2);
+        save_tsdg(g, "/tmp/tsdg_gpu_api.tsdg");
+        const auto g2 = load_tsdg("/tmp/tsdg_gpu_api.tsdg");
+        BestFirstParams p;
+        p.k = 10;
+        p.seed = 5;
+        CHECK(gpu::large_batch_search(g2, base, queries, p) == large_batch_search(g, base, queries, p));
+        std::remove("/tmp/tsdg_gpu_api.tsdg");
+    }
+    std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
+    return g_fail;
+}
