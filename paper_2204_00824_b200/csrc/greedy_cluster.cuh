@@ -1,0 +1,276 @@
+// Small-batch multi-start greedy search (paper Alg. 1), latency-oriented form:
+// one CTA per (query, walk), one thread-block CLUSTER per query.
+//
+// Inside a CTA, one hop's lambda-prefix (up to deg_cut[u] edges) is spread over
+// the CTA's warps: warp w evaluates groups w, w+W, ... of 32 edges (lane = edge
+// position mod 32, exactly the reference's lane mapping, greedy_search.cpp:49-58)
+// and keeps its per-lane strict-< minimum together with the group index; the
+// partials are combined in shared memory as min-by-(dist, group) — the
+// reference's sequential lane_update over groups in order (rank_list.cpp:8-18)
+// lets an earlier group keep a tie, which is exactly "smaller group wins".  Warp 0
+// then runs merge_halves / next-node selection (warp_merge_halves) and the hop
+// loop continues with the whole CTA.
+//
+// The t0 walks of a query run on the t0 CTAs of one cluster (t0 <= 16; 8 is the
+// portable limit, up to 16 with the non-portable attribute).  When all walks are
+// done, CTA rank 0 reads every walk's 32-slot R_ij from its siblings' shared
+// memory over DSMEM, pools the finite entries, sorts by (dist, id), drops
+// adjacent duplicate ids and writes the first k (greedy_search.cpp:85-103) — no
+// second kernel, no global round trip.  For t0 > 16 the same kernel writes the
+// walks to global memory and greedy_merge_kernel finishes.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "greedy.cuh"
+
+namespace tsdg_dev {
+
+namespace cg = cooperative_groups;
+
+constexpr int kGcWarps = 4;
+constexpr int kGcThreads = kGcWarps * 32;
+
+struct GcArgs {
+    const float* vec;
+    const uint32_t* adj;
+    const uint32_t* degcut;
+    const float* queries;
+    uint32_t ld, R, n, d;
+    uint32_t nq, t0, hop_limit, k;
+    uint64_t seed;
+    const uint64_t* walk_states;  // optional explicit RNG state per walk
+    uint32_t* out_ids;
+    float* out_dists;
+    uint32_t* out_counts;
+    tsdg_query_stats* out_stats;
+    uint32_t* walk_ids;  // non-cluster mode
+    float* walk_dists;
+    uint32_t* walk_hops;
+    uint32_t* walk_evals;
+    int cluster;         // 1: the t0 CTAs of a query form one cluster
+    uint32_t npow2;      // pool size for the in-cluster merge
+    uint32_t dch, slots;
+    uint32_t off_query, off_stage, off_part, off_bar, off_ctl, off_list, off_pool;
+};
+
+struct GcPart {
+    float d;
+    uint32_t id;
+    uint32_t group;
+    uint32_t pad;
+};
+
+struct GcCtl {
+    uint32_t u;
+    uint32_t improved;
+    uint32_t hops;
+    uint32_t evals;
+};
+
+template <int METRIC, bool FAST>
+__global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t walk = blockIdx.x;
+    const uint32_t q = walk / a.t0, s = walk % a.t0;
+    float* sq = reinterpret_cast<float*>(smem_raw + a.off_query);
+    GcPart* part = reinterpret_cast<GcPart*>(smem_raw + a.off_part);
+    GcCtl* ctl = reinterpret_cast<GcCtl*>(smem_raw + a.off_ctl);
+    float* list_d = reinterpret_cast<float*>(smem_raw + a.off_list);
+    uint32_t* list_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_list + 32 * 4);
+    const uint32_t pitch = a.dch + 4;
+    WarpStage w;
+    w.sq = sq;
+    w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * pitch;
+    w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
+    w.parity = 0;
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
+    const float kInf = __int_as_float(0x7f800000);
+
+    const float* gq = a.queries + (size_t)q * a.d;
+    for (uint32_t i = threadIdx.x; i < a.ld; i += blockDim.x) sq[i] = i < a.d ? gq[i] : 0.0f;
+    if (lane == 0) mbar_init(w.bar, 1);
+    __syncthreads();
+
+    // select_start (greedy_search.cpp:12-25) by warp 0
+    if (warp == 0) {
+        const uint64_t st = a.walk_states ? a.walk_states[walk] : fork_state(a.seed, s);
+        const uint32_t v = draw_below(st, (uint32_t)lane, a.n);
+        float sd = gather_eval<METRIC, FAST, kStageTma>(w, g, true, v, lane);
+        uint32_t si = v;
+        warp_argmin(sd, si);
+        if (lane == 0) {
+            ctl->u = si;
+            ctl->improved = 1;
+            ctl->hops = 0;
+            ctl->evals = 32;
+        }
+    }
+    __syncthreads();
+
+    float rd = kInf;  // R_ij slot `lane` (warp 0)
+    uint32_t ri = kInvalid;
+    uint32_t t = 0;
+    while (ctl->improved && t < a.hop_limit) {
+        ++t;
+        const uint32_t u = ctl->u;
+        const uint32_t deg = __ldg(a.degcut + u);
+        const uint32_t* arow = a.adj + (size_t)u * a.R;
+        const uint32_t ngroups = (deg + 31) / 32;
+        float md = kInf;
+        uint32_t mi = kInvalid, mg = 0xFFFFFFFFu;
+        for (uint32_t gi = warp; gi < ngroups; gi += kGcWarps) {
+            const uint32_t j = gi * 32 + lane;
+            const bool valid = j < deg;
+            const uint32_t e = valid ? __ldg(arow + j) : kInvalid;
+            const float dist = gather_eval<METRIC, FAST, kStageTma>(w, g, valid, e, lane);
+            if (valid && dist < md) {
+                md = dist;
+                mi = e;
+                mg = gi;
+            }
+        }
+        part[warp * 32 + lane] = GcPart{md, mi, mg, 0};
+        __syncthreads();
+        if (warp == 0) {
+            float td = kInf;
+            uint32_t ti = kInvalid, tg = 0xFFFFFFFFu;
+            for (int ww = 0; ww < kGcWarps; ++ww) {
+                const GcPart p = part[ww * 32 + lane];
+                if (p.id == kInvalid) continue;
+                if (p.d < td || (p.d == td && p.group < tg)) {
+                    td = p.d;
+                    ti = p.id;
+                    tg = p.group;
+                }
+            }
+            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
+            float nd = td;
+            uint32_t ni = ti;
+            warp_argmin(nd, ni);
+            if (lane == 0) {
+                if (ni != kInvalid) ctl->u = ni;
+                ctl->improved = updated ? 1u : 0u;
+                ctl->evals += deg;
+            }
+        }
+        __syncthreads();
+    }
+
+    if (!a.cluster) {
+        if (warp == 0) {
+            a.walk_ids[(size_t)walk * 32 + lane] = ri;
+            a.walk_dists[(size_t)walk * 32 + lane] = rd;
+            if (lane == 0) {
+                a.walk_hops[walk] = t;
+                a.walk_evals[walk] = ctl->evals;
+            }
+        }
+        return;
+    }
+
+    // ---- in-cluster merge over DSMEM (CTA rank 0 of the query's cluster) ---------
+    if (warp == 0) {
+        list_d[lane] = rd;
+        list_i[lane] = ri;
+        if (lane == 0) ctl->hops = t;
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (cluster.block_rank() == 0) {
+        float* pd = reinterpret_cast<float*>(smem_raw + a.off_pool);
+        uint32_t* pi = reinterpret_cast<uint32_t*>(smem_raw + a.off_pool + a.npow2 * 4);
+        uint32_t* scan = pi + a.npow2;  // blockDim + 1
+        const uint32_t total = a.t0 * 32;
+        for (uint32_t i = threadIdx.x; i < a.npow2; i += blockDim.x) {
+            float dd = kInf;
+            uint32_t id = kInvalid;
+            if (i < total) {
+                const uint32_t r = i / 32, slot = i % 32;
+                const float* rl = cluster.map_shared_rank(list_d, r);
+                const uint32_t* il = cluster.map_shared_rank(list_i, r);
+                id = il[slot];
+                dd = id != kInvalid ? rl[slot] : kInf;
+            }
+            pd[i] = dd;
+            pi[i] = id;
+        }
+        uint32_t hsum = 0, esum = 0;
+        if (threadIdx.x == 0) {
+            for (uint32_t r = 0; r < a.t0; ++r) {
+                const GcCtl* rc = cluster.map_shared_rank(ctl, r);
+                hsum += rc->hops;
+                esum += rc->evals;
+            }
+        }
+        __syncthreads();
+        for (uint32_t kk = 2; kk <= a.npow2; kk <<= 1) {
+            for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < a.npow2; i += blockDim.x) {
+                    const uint32_t p = i ^ j;
+                    if (p > i) {
+                        const bool up = (i & kk) == 0;
+                        const bool p_first = closer(pd[p], pi[p], pd[i], pi[i]);
+                        if (p_first == up) {
+                            const float td = pd[i];
+                            const uint32_t ti = pi[i];
+                            pd[i] = pd[p];
+                            pi[i] = pi[p];
+                            pd[p] = td;
+                            pi[p] = ti;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const uint32_t per = (a.npow2 + blockDim.x - 1) / blockDim.x;
+        const uint32_t b0 = threadIdx.x * per;
+        uint32_t cnt = 0;
+        for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i)
+            cnt += (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) ? 1u : 0u;
+        scan[threadIdx.x] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (uint32_t x = 0; x < blockDim.x; ++x) {
+                const uint32_t c = scan[x];
+                scan[x] = run;
+                run += c;
+            }
+            scan[blockDim.x] = run;
+        }
+        __syncthreads();
+        uint32_t pos = scan[threadIdx.x];
+        for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i) {
+            if (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) {
+                if (pos < a.k) {
+                    a.out_ids[(size_t)q * a.k + pos] = pi[i];
+                    if (a.out_dists) a.out_dists[(size_t)q * a.k + pos] = pd[i];
+                }
+                ++pos;
+            }
+        }
+        const uint32_t uniq = scan[blockDim.x];
+        const uint32_t c = uniq < a.k ? uniq : a.k;
+        for (uint32_t i = c + threadIdx.x; i < a.k; i += blockDim.x) {
+            a.out_ids[(size_t)q * a.k + i] = kInvalid;
+            if (a.out_dists) a.out_dists[(size_t)q * a.k + i] = kInf;
+        }
+        if (threadIdx.x == 0) {
+            if (a.out_counts) a.out_counts[q] = c;
+            if (a.out_stats) {
+                tsdg_query_stats st;
+                st.hops = hsum;
+                st.distance_evals = esum;
+                st.queue_evictions = 0;
+                st.edges_examined = esum - 32u * a.t0;
+                a.out_stats[q] = st;
+            }
+        }
+    }
+    cluster.sync();  // siblings stay resident until rank 0 has read their lists
+}
+
+}  // namespace tsdg_dev

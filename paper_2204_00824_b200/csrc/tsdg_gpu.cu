@@ -20,7 +20,7 @@
 #include <vector>
 
 #include "../../include/tsdg_gpu.h"
-#include "greedy.cuh"
+#include "greedy_cluster.cuh"
 
 using namespace tsdg_dev;
 
@@ -153,7 +153,7 @@ void fill_bf_layout(BfArgs& a) {
 
 // Tuning knobs (environment, read per launch): TSDG_STAGE=tma (default)|ldgsts,
 // TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency, 4: speculative
-// next-hop adjacency; default 4),
+// next-hop adjacency; default 0: measured slower on C2, see profiles/),
 // TSDG_BF_WARPS=<warps per CTA> (default 1: finest shared-memory granularity),
 // TSDG_SLOTS=<staged rows per gather round> (default 16).
 int env_int(const char* name, int dflt) {
@@ -229,7 +229,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.work_counter = next_counter(idx, st);
     a.dch = staging_dims(idx->ld);
     a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
-    a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 4);
+    a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
     fill_bf_layout(a);
     const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
     const size_t smem = (size_t)a.warp_smem * wpc;
@@ -325,13 +325,112 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
 }
 
+// CTA-per-walk / cluster-per-query greedy (greedy_cluster.cuh).  Returns false when
+// the cluster launch is not possible (then the caller merges walks itself).
+bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
+                       const tsdg_greedy_params* p, bool fast, const uint64_t* d_states,
+                       uint32_t* d_ids, float* d_dists, uint32_t* d_counts,
+                       tsdg_query_stats* d_stats, WalkBuffers* wb, cudaStream_t st) {
+    GcArgs a{};
+    a.vec = idx->vec;
+    a.adj = idx->adj;
+    a.degcut = get_degcut(idx, p->lambda_cut, st);
+    a.queries = d_queries;
+    a.ld = idx->ld;
+    a.R = idx->R;
+    a.n = idx->n;
+    a.d = idx->d;
+    a.nq = nq;
+    a.t0 = p->t0;
+    a.hop_limit = p->hop_limit;
+    a.k = k;
+    a.seed = p->seed;
+    a.walk_states = d_states;
+    a.out_ids = d_ids;
+    a.out_dists = d_dists;
+    a.out_counts = d_counts;
+    a.out_stats = d_stats;
+    a.cluster = (wb == nullptr) ? 1 : 0;
+    if (wb) {
+        a.walk_ids = wb->ids;
+        a.walk_dists = wb->dists;
+        a.walk_hops = wb->hops;
+        a.walk_evals = wb->evals;
+    }
+    a.npow2 = 32;
+    while (a.npow2 < p->t0 * 32) a.npow2 <<= 1;
+    a.dch = staging_dims(idx->ld);
+    a.slots = 32;
+    Carve c;
+    a.off_bar = c.take(8 * kGcWarps, 8);
+    a.off_ctl = c.take(sizeof(GcCtl));
+    a.off_list = c.take(32 * 8);
+    a.off_query = c.take(a.ld * 4);
+    a.off_part = c.take(kGcThreads * sizeof(GcPart));
+    a.off_stage = c.take(kGcWarps * a.slots * (a.dch + 4) * 4, 128);
+    a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 : 0);
+    const size_t smem = round_up(c.total, 128);
+    using GcKernel = void (*)(GcArgs);
+    GcKernel kern;
+    if (idx->metric == 0) kern = fast ? greedy_cta_kernel<0, true> : greedy_cta_kernel<0, false>;
+    else if (idx->metric == 1) kern = fast ? greedy_cta_kernel<1, true> : greedy_cta_kernel<1, false>;
+    else kern = fast ? greedy_cta_kernel<2, true> : greedy_cta_kernel<2, false>;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute(greedy_cta)");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nq * p->t0);
+    cfg.blockDim = dim3(kGcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (a.cluster) {
+        if (p->t0 > 8)
+            cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                       "cudaFuncSetAttribute(non-portable cluster)");
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = p->t0;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "greedy_cta_kernel launch");
+    g_launches++;
+    return true;
+}
+
+// Kernel choice for Alg. 1: the latency-oriented CTA/cluster kernel for small
+// batches (the paper's small-batch regime), the warp-per-walk
+// kernel when there are enough walks to fill the GPU.  TSDG_GREEDY=cta|warp forces.
+bool use_cta_greedy(const tsdg_gpu_index* idx, uint32_t nq, uint32_t t0) {
+    if (env_is("TSDG_GREEDY", "cta")) return true;
+    if (env_is("TSDG_GREEDY", "warp")) return false;
+    return (uint64_t)nq * t0 <= 8ull * idx->sm_count;
+}
+
 void launch_greedy(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
                    const tsdg_greedy_params* p, int mode, uint32_t* d_ids, float* d_dists,
                    uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
     if (nq == 0) return;
+    const bool fast = mode == TSDG_MODE_FAST;
+    const bool cta = use_cta_greedy(idx, nq, p->t0);
+    if (cta && p->t0 <= 16 &&
+        launch_greedy_cta(idx, d_queries, nq, k, p, fast, nullptr, d_ids, d_dists, d_counts,
+                          d_stats, nullptr, st))
+        return;
     WalkBuffers wb = alloc_walks(nq * p->t0, st);
-    launch_walks(idx, d_queries, nq, p->t0, p->hop_limit, p->lambda_cut, p->seed, nullptr, wb, st,
-                 mode == TSDG_MODE_FAST);
+    if (cta) {
+        launch_greedy_cta(idx, d_queries, nq, k, p, fast, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, &wb, st);
+    } else {
+        launch_walks(idx, d_queries, nq, p->t0, p->hop_limit, p->lambda_cut, p->seed, nullptr, wb,
+                     st, fast);
+    }
     uint32_t npow2 = 32;
     while (npow2 < p->t0 * 32) npow2 <<= 1;
     const size_t smem = (size_t)npow2 * 8 + (kMergeThreads + 1) * 4;

@@ -280,3 +280,26 @@ def test_c1_fast_mode_recall(orc):
         assert abs(rf - rd) <= 0.005, (k, rf, rd)
         rel = np.abs(fast.dists[:, :1] - det.dists[:, :1]) / np.maximum(det.dists[:, :1], 1e-30)
         assert np.nanmax(rel) < 1e-4
+
+
+@pytest.mark.parametrize("kernel", ["cta", "warp"])
+def test_greedy_kernels_bit_exact(orc, fixtures, index, golden, golden_meta, monkeypatch, kernel):
+    """Both Alg. 1 kernels (CTA/cluster-per-query and warp-per-walk) reproduce the
+    reference, including t0 > 16 (no cluster: walks merged by greedy_merge_kernel)."""
+    monkeypatch.setenv("TSDG_GREEDY", kernel)
+    for name in FIXTURES:
+        g, b, q = fixtures(name)
+        idx = index(name)
+        for i, gd in enumerate(golden_meta["gr_grid"]):
+            p = GreedyParams(**{k: v for k, v in gd.items() if k != "k"})
+            got = idx.search_greedy(q[:64], gd["k"], p)
+            np.testing.assert_array_equal(got.ids, golden[f"{name}_gr{i}_ids"][:64])
+            np.testing.assert_array_equal(got.stats["hops"], golden[f"{name}_gr{i}_stats"][:64, 0])
+            np.testing.assert_array_equal(got.stats["distance_evals"],
+                                          golden[f"{name}_gr{i}_stats"][:64, 1])
+        for t0 in (8, 24):
+            p = GreedyParams(t0=t0, seed=3)
+            got = idx.search_greedy(q[:16], 10, p)
+            want = orc.small_batch(g, b, q[:16], 10, p)
+            np.testing.assert_array_equal(got.ids, want.ids)
+            np.testing.assert_array_equal(got.dists.view(np.uint32), want.dists.view(np.uint32))
