@@ -410,7 +410,7 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
 bool use_cta_greedy(const tsdg_gpu_index* idx, uint32_t nq, uint32_t t0) {
     if (env_is("TSDG_GREEDY", "cta")) return true;
     if (env_is("TSDG_GREEDY", "warp")) return false;
-    return (uint64_t)nq * t0 <= 8ull * idx->sm_count;
+    return (uint64_t)nq * t0 <= 2ull * idx->sm_count;  // measured crossover, C2 (profiles/)
 }
 
 void launch_greedy(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
