@@ -126,6 +126,167 @@ def profiled_traffic(mode: str):
         return None
 
 
+SHARDED = "c5s_lowlid_2m_96"
+C4 = "c4_lowlid_1m_960"
+
+
+def _events_time(fn, steps, stream=None):
+    import torch
+    evs = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def small_batch_section(idx, ds, dev):
+    """Alg. 1 (greedy, CTA/cluster kernel for small batches) latency on C2:
+    batch 1 / 8 / 64, t0 = 16 (recall@10 >= 0.95), queries resident on the device."""
+    import torch
+
+    from oracle.oracle import recall_at_k
+    from paper_2204_00824_b200.search import GreedyParams
+
+    out = []
+    p = GreedyParams(t0=16, hop_limit=16, lambda_cut=10, seed=7)
+    k = 10
+    for batch in (1, 8, 64):
+        reps = 256 if batch == 1 else 1024 // batch
+        dq = torch.from_numpy(ds.queries[:reps * batch]).to(dev)
+        ids = torch.empty((reps * batch, k), dtype=torch.int32, device=dev)
+        dd = torch.empty((reps * batch, k), dtype=torch.float32, device=dev)
+        cc = torch.empty(reps * batch, dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+
+        def call(j):
+            idx.search_greedy_device(dq[j * batch].data_ptr(), batch, k, p, ids[j * batch].data_ptr(),
+                                     dd[j * batch].data_ptr(), cc[j * batch].data_ptr(), 0, st)
+
+        for j in range(3):
+            call(j)
+        torch.cuda.synchronize()
+        times = []
+        for j in range(reps):  # one call at a time: latency, not throughput
+            times += _events_time(lambda: call(j), 1)
+        rec = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(),
+                          ds.gt[:reps * batch], 10)
+        lat = float(np.median(times))
+        out.append({"batch": batch, "t0": p.t0, "latency_ms_p50": lat,
+                    "latency_ms_p99": float(np.percentile(times, 99)),
+                    "qps": batch / lat * 1e3, "recall_at_10": rec})
+    return {"procedure": "greedy (paper Alg. 1), deterministic, C2 index", "points": out}
+
+
+def sharded_section(args, ws, rank, local, dev, dist):
+    """Sharded base (C5 shape, scaled to 2M x 96 in 8 shards): each rank searches all
+    queries on its 8/N shards, NCCL all-gather of per-shard top-k, device merge."""
+    from paper_2204_00824_b200 import _native, datasets, shards
+    from paper_2204_00824_b200.search import BestFirstParams, load_tsdg
+
+    import torch
+
+    d = os.path.join(datasets.DATA_DIR, SHARDED)
+    if not os.path.exists(os.path.join(d, "meta.json")):
+        return {"unavailable": f"data/{SHARDED} missing (tools/make_sharded.py)"}
+    with open(os.path.join(d, "meta.json")) as f:
+        meta = json.load(f)
+    if 8 % ws:
+        return {"unavailable": f"8 shards do not split over {ws} GPUs"}
+    base, queries = datasets.generate(meta["spec"])
+    table = [(s["offset"], s["n"]) for s in meta["shards"]]
+    mine = shards.shards_of_rank(len(table), ws, rank)
+    graphs, bases = {}, {}
+    from tools import graph_pack
+    for s in mine:
+        path = os.path.join(d, f"shard_{s}.tsdg")
+        off, n = table[s]
+        if not os.path.exists(path):
+            graph_pack.unpack(os.path.join(d, f"shard_{s}.pack.npz"), base[off:off + n], path)
+        graphs[s] = load_tsdg(path)
+        bases[s] = base[off:off + n]
+    searcher = shards.ShardedSearcher(graphs, bases, table, device=local,
+                                      group=dist.group.WORLD if ws > 1 else None)
+    p = BestFirstParams(k=16, seed=7)
+    qd = torch.from_numpy(queries).to(dev)
+    mode = _native.MODE_FAST if args.mode == "fast" else _native.MODE_DETERMINISTIC
+    for _ in range(3):
+        ids, dists, counts = searcher.search(qd, p, mode=mode)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    steps = max(5, args.steps // 2)
+    times = _events_time(lambda: searcher.search(qd, p, mode=mode), steps)
+    total = sum(times) / 1e3
+    if ws > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    ids, dists, counts = searcher.search(qd, p, mode=mode)
+    from oracle.oracle import recall_at_k
+    gt = np.fromfile(os.path.join(d, "gt.u32"), np.uint32).reshape(meta["gt_queries"], meta["gt_k"])
+    nq_gt = gt.shape[0]
+    rec = recall_at_k(ids[:nq_gt].cpu().numpy().view(np.uint32), counts[:nq_gt].cpu().numpy(), gt, 10)
+    nq = queries.shape[0]
+    return {"workload": f"{meta['spec']['n']}x{meta['spec']['d']} fp32 in {len(table)} shards "
+                        "(Deep100M-shape scaled 50x), TSDG per shard from the reference builder",
+            "params": {"k": p.k, "lambda_cut": p.lambda_cut, "m_segments": p.m_segments,
+                       "delta": p.delta, "seed": p.seed}, "mode": args.mode,
+            "n_gpus": ws, "shards_per_gpu": len(mine), "queries": nq,
+            "value": nq * steps / total, "unit": "queries/s (every query searched on all shards)",
+            "ms_per_step": total / steps * 1e3, "recall_at_10": rec,
+            "collective": "all_gather_into_tensor (NCCL) of per-shard (ids, dists, counts)" if ws > 1 else "none (1 GPU)"}
+
+
+def c4_section(args, dev):
+    """GIST1M shape (1M x 960 fp32), batch 10K, replicated index, one GPU."""
+    import torch
+
+    from oracle.oracle import recall_at_k
+    from paper_2204_00824_b200 import _native, datasets
+    from paper_2204_00824_b200.search import BestFirstParams, GpuIndex, load_tsdg
+
+    if not datasets.available(C4):
+        return {"unavailable": f"data/{C4} missing (tools/make_dataset.py --d 960)"}
+    ds = datasets.load(C4)
+    idx = GpuIndex(load_tsdg(ds.graph_path), ds.base, device=dev.index or 0)
+    nq = ds.queries.shape[0]
+    dq = torch.from_numpy(ds.queries).to(dev)
+    best = None
+    for k in (10, 16, 24, 32):
+        p = BestFirstParams(k=k, seed=7)
+        ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        dd = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        cc = torch.empty(nq, dtype=torch.int32, device=dev)
+        stt = torch.empty((nq, 4), dtype=torch.int32, device=dev)
+        mode = _native.MODE_FAST if args.mode == "fast" else _native.MODE_DETERMINISTIC
+        st = torch.cuda.current_stream(dev).cuda_stream
+
+        def call():
+            idx.search_bestfirst_device(dq.data_ptr(), nq, p, ids.data_ptr(), dd.data_ptr(),
+                                        cc.data_ptr(), stt.data_ptr(), st, mode=mode)
+
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize()
+        rec = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(), ds.gt, 10)
+        times = _events_time(call, 5)
+        s = stt.cpu().numpy().astype(np.int64)
+        alg = 4 * 960 * s[:, 1].sum() + 4 * s[:, 3].sum() + nq * (4 * 960 + 8 * k)
+        ms = float(np.median(times))
+        best = {"k_search": k, "recall_at_10": rec, "value": nq / ms * 1e3, "unit": "queries/s",
+                "ms_per_batch": ms, "roofline_achieved_GBps": alg / ms / 1e6,
+                "roofline_frac": alg / ms / 1e6 / peaks()[0]}
+        if rec >= 0.95:
+            break
+    idx.close()
+    return {"workload": "GIST1M-shaped 1M x 960 fp32 L2 low-LID (latent 26), batch 10K, "
+                        "TSDG from the reference builder (nn_descent k=64)", **best}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,6 +363,8 @@ def main():
     ap.add_argument("--ref-queries", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["det", "fast"], default="fast")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the small-batch / sharded / C4 secondary measurements")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
@@ -325,6 +488,20 @@ def main():
     e2e_val = nq * ws * args.steps / e2e_s
     assert np.array_equal(h_ids.numpy().view(np.uint32), head["ids"]), "e2e result differs"
 
+    # ---- secondary workloads (not the headline): small batch, sharded base, C4 -----
+    extras = {}
+    if not args.no_extras:
+        del flush
+        torch.cuda.empty_cache()
+        if rank == 0:
+            extras["small_batch"] = small_batch_section(idx, ds, dev)
+        extras["sharded"] = sharded_section(args, ws, rank, local, dev, dist)
+        if rank == 0:
+            idx.close()
+            del dq, d_ids, d_dists, d_counts, d_stats
+            torch.cuda.empty_cache()
+            extras["c4_gist_shape"] = c4_section(args, dev)
+
     if rank == 0:
         peak, peak_kind = peaks()
         achieved = head["alg_bytes"] / kernel_s / 1e9
@@ -367,6 +544,7 @@ def main():
             "gpu_launches": head["launches"],
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            **extras,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
