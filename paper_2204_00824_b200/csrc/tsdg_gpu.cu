@@ -21,6 +21,7 @@
 
 #include "../../include/tsdg_gpu.h"
 #include "greedy_cluster.cuh"
+#include "unbounded.cuh"
 
 using namespace tsdg_dev;
 
@@ -68,6 +69,14 @@ struct DeviceGuard {
 };
 
 uint32_t round_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+template <class T>
+T* dev_alloc(size_t count, cudaStream_t st) {
+    T* p = nullptr;
+    if (count == 0) count = 1;
+    cuda_check(cudaMallocAsync(&p, sizeof(T) * count, st), "cudaMallocAsync");
+    return p;
+}
 
 }  // namespace
 
@@ -195,17 +204,90 @@ void validate_bf(const tsdg_gpu_index* idx, const tsdg_bf_params* p) {
     if (p->k < 1 || p->hop_limit < 1 || p->m_segments < 1 || p->lambda_cut < 1 ||
         p->delta < 0.0f || std::isnan(p->delta))
         fail(TSDG_EINVAL, "bestfirst_search: invalid parameters");
-    if (p->unbounded)
-        fail(TSDG_EINVAL, "bestfirst_search: unbounded=true (exact std::set queue) is not "
-                          "implemented on the GPU path");
-    if (p->m_segments > 32) fail(TSDG_EINVAL, "bestfirst_search: GPU path supports m_segments <= 32");
+    if (!p->unbounded && p->m_segments > 32)
+        fail(TSDG_EINVAL, "bestfirst_search: GPU path supports m_segments <= 32");
     if (p->k > 1024) fail(TSDG_EINVAL, "bestfirst_search: GPU path supports k <= 1024");
+}
+
+// unbounded=true: exact queue / visited set (unbounded.cuh), per-warp arena in HBM
+void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint64_t qbase,
+                      const tsdg_bf_params* p, int mode, uint32_t* d_ids, float* d_dists,
+                      uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
+    UbArgs a{};
+    a.vec = idx->vec;
+    a.adj = idx->adj;
+    a.degcut = get_degcut(idx, p->lambda_cut, st);
+    a.queries = d_queries;
+    a.ld = idx->ld;
+    a.R = idx->R;
+    a.n = idx->n;
+    a.d = idx->d;
+    a.nq = nq;
+    a.qbase = qbase;
+    a.k = p->k;
+    a.hop_limit = p->hop_limit;
+    a.delta = p->delta;
+    a.seed = p->seed;
+    a.out_ids = d_ids;
+    a.out_dists = d_dists;
+    a.out_counts = d_counts;
+    a.out_stats = d_stats;
+    a.work_counter = next_counter(idx, st);
+    a.dch = staging_dims(idx->ld);
+    a.slots = 32;
+    // every id the search can touch: <= min(n, 1 + hop_limit * max degree)
+    const uint64_t touch = std::min<uint64_t>(idx->n, 1ull + (uint64_t)p->hop_limit * idx->max_degree) + 32;
+    uint64_t hcap = 64;
+    while (hcap < 2 * touch + 2) hcap <<= 1;
+    a.hcap = (uint32_t)hcap;
+    a.qcap = (uint32_t)(touch + 2);
+    const size_t per_warp = hcap * 5 + (size_t)a.qcap * 8 + (size_t)(p->k + 2) * 8;
+    const size_t budget = size_t(2) << 30;
+    uint32_t warps = (uint32_t)std::max<size_t>(1, std::min<size_t>(budget / per_warp, 4u * idx->sm_count));
+    warps = std::min(warps, nq);
+    char* arena = dev_alloc<char>(per_warp * warps + 256, st);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* r = arena + off; off += (bytes + 15) & ~size_t(15); return r; };
+    a.hkeys = reinterpret_cast<uint32_t*>(take(hcap * 4 * warps));
+    a.hstate = reinterpret_cast<uint8_t*>(take(hcap * warps));
+    a.heap_d = reinterpret_cast<float*>(take((size_t)a.qcap * 4 * warps));
+    a.heap_i = reinterpret_cast<uint32_t*>(take((size_t)a.qcap * 4 * warps));
+    a.rid = reinterpret_cast<uint32_t*>(take((size_t)(p->k + 2) * 4 * warps));
+    a.rdist = reinterpret_cast<float*>(take((size_t)(p->k + 2) * 4 * warps));
+    int* over = dev_alloc<int>(1, st);
+    cuda_check(cudaMemsetAsync(over, 0, sizeof(int), st), "memset");
+    a.overflow = over;
+    Carve c;
+    a.off_bar = c.take(8, 8);
+    a.off_query = c.take(a.ld * 4);
+    a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
+    a.warp_smem = round_up(c.total, 128);
+    void (*kern)(UbArgs);
+    const bool fast = mode == TSDG_MODE_FAST;
+    if (idx->metric == 0) kern = fast ? bf_unbounded_kernel<0, true> : bf_unbounded_kernel<0, false>;
+    else if (idx->metric == 1) kern = fast ? bf_unbounded_kernel<1, true> : bf_unbounded_kernel<1, false>;
+    else kern = fast ? bf_unbounded_kernel<2, true> : bf_unbounded_kernel<2, false>;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.warp_smem),
+               "cudaFuncSetAttribute(unbounded)");
+    kern<<<warps, 32, a.warp_smem, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "bf_unbounded_kernel launch");
+    int h_over = 0;
+    cuda_check(cudaMemcpyAsync(&h_over, over, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    cudaFreeAsync(arena, st);
+    cudaFreeAsync(over, st);
+    cuda_check(cudaStreamSynchronize(st), "bf_unbounded_kernel");
+    if (h_over) fail(TSDG_ERUNTIME, "bestfirst_search(unbounded): arena capacity exceeded");
 }
 
 void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint64_t qbase,
                       const tsdg_bf_params* p, int mode, uint32_t* d_ids, float* d_dists,
                       uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
     if (nq == 0) return;
+    if (p->unbounded) {
+        launch_unbounded(idx, d_queries, nq, qbase, p, mode, d_ids, d_dists, d_counts, d_stats, st);
+        return;
+    }
     BfArgs a{};
     a.vec = idx->vec;
     a.adj = idx->adj;
@@ -459,13 +541,6 @@ void check_cosine_queries(const tsdg_gpu_index* idx, const float* queries, uint3
     }
 }
 
-template <class T>
-T* dev_alloc(size_t count, cudaStream_t st) {
-    T* p = nullptr;
-    if (count == 0) count = 1;
-    cuda_check(cudaMallocAsync(&p, sizeof(T) * count, st), "cudaMallocAsync");
-    return p;
-}
 
 }  // namespace
 
