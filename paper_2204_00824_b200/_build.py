@@ -43,6 +43,17 @@ def build_gpu(force: bool = False) -> str:
     return out
 
 
+def build_gpu_phases(force: bool = False) -> str:
+    """Development variant with per-phase clock64 counters (-DTSDG_PHASES)."""
+    out = os.path.join(LIB, "libtsdg_gpu_phases.so")
+    srcs = [os.path.join(CSRC, f) for f in ("tsdg_gpu.cu", "tsdg_io.cpp")]
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    if force or _stale(out, deps):
+        _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-DTSDG_PHASES", "-Xcompiler",
+              "-fPIC,-O2", "-shared", "-o", out, *srcs])
+    return out
+
+
 def build_datagen(force: bool = False) -> str:
     os.makedirs(LIB, exist_ok=True)
     out = os.path.join(LIB, "libtsdg_datagen.so")
@@ -69,4 +80,5 @@ def build_all(force: bool = False) -> None:
     build_datagen(force)
     build_oracle()
     build_gpu(force)
+    build_gpu_phases(force)
     build_cpp_tests()

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtsdg_gpu.so")
+LIB_PATH = os.environ.get("TSDG_LIB") or os.path.join(_HERE, "_lib", "libtsdg_gpu.so")
 
 TSDG_OK, TSDG_EINVAL, TSDG_ERUNTIME, TSDG_ENCCL = 0, 1, 2, 3
 MODE_DETERMINISTIC, MODE_FAST = 0, 1

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
 
         uint32_t hops = 0, evals = 0, evictions = 0, examined = 0, ctotal = 0, rn = 0;
         RReg rr{kInf, kInvalid};
+        PH_DECL
 
         // 32 uniform start draws with replacement; best by closer (:57-63)
         const uint64_t s0 = fork_state(a.seed, a.qbase + q);
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
         else r_push_smem(w, rn, si, sd, lane);
         c_push(w, a.m, si, sd, ctotal, evictions, lane);
         float rfar = KREG ? __shfl_sync(kFull, rr.d, rn - 1) : w.rdist[rn - 1];
+        PH_MARK(0)
         // speculative next expansion (see below): its deg + first 64 adjacency entries
         uint32_t spec_u = kInvalid, spec_deg = 0, spec_e0 = kInvalid, spec_e1 = kInvalid;
 
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
             spec_u = kInvalid;
             v_add(w, a.m, u, lane);
             examined += deg;
+            PH_MARK(1)
             for (uint32_t base = 0; base < deg; base += 32) {
                 const uint32_t j = base + lane;
                 const bool valid = j < deg;
@@ -366,7 +369,9 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
                     const bool nv = base + 32 + lane < deg && !v_contains(w, a.m, e_next);
                     prefetch_rows(a, nv, e_next);
                 }
+                PH_MARK(2)
                 float dist = gather_eval<METRIC, FAST, STAGE>(w.st, g, need, e, lane);
+                PH_RESET
                 if (spec && base + 32 >= deg) {
                     // Last chunk of the hop: the next pop is C's minimum after these
                     // admissions = closer of (current C head, best candidate passing the
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
                         }
                     }
                 }
+                PH_MARK(5)
             }
         }
 

@@ -15,6 +15,26 @@
 
 namespace tsdg_dev {
 
+// Phase-cycle instrumentation (development build only: -DTSDG_PHASES builds
+// libtsdg_gpu_phases.so; tools/phase_profile.py reads the counters).  Each warp
+// accumulates clock64() deltas per phase into its own slot.
+#ifdef TSDG_PHASES
+__device__ unsigned long long g_phase[1 << 16][8];
+__device__ __forceinline__ unsigned gwarp_id() { return (blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
+#define PH_DECL long long _ph = clock64();
+#define PH_RESET _ph = clock64();
+#define PH_MARK(i)                                                                      \
+    {                                                                                   \
+        const long long _n = clock64();                                                 \
+        if ((threadIdx.x & 31) == 0) tsdg_dev::g_phase[tsdg_dev::gwarp_id() & 0xFFFF][i] += _n - _ph; \
+        _ph = _n;                                                                       \
+    }
+#else
+#define PH_DECL
+#define PH_RESET
+#define PH_MARK(i)
+#endif
+
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;

@@ -146,6 +146,7 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
     const float kInf = __int_as_float(0x7f800000);
     const unsigned nm = __ballot_sync(kFull, need);
     if (nm == 0) return kInf;
+    PH_DECL
     const uint32_t pitch = g.dch + 4;
     const uint32_t cnt = __popc(nm);
     const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
@@ -173,6 +174,7 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
                 if (mine_round) bulk_g2s(w.stage + slot * pitch, row_src + c0, cw * 4u, w.bar);
                 mbar_wait(w.bar, w.parity);
                 w.parity ^= 1u;
+                PH_MARK(3)
             } else {
                 __syncwarp();
                 const uint32_t nvec = cw >> 2;             // 16-byte pieces per row
@@ -227,6 +229,7 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
             dist = finish_exact<METRIC>(acc);
         }
         const float got = __shfl_sync(kFull, dist, (int)(slot & 31u));
+        PH_MARK(4)
         if (mine_round) result = got;
     }
     return result;

@@ -907,3 +907,19 @@ int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
 }
 
 }  // extern "C"
+
+#ifdef TSDG_PHASES
+// Development build only: per-phase cycle totals summed over warps (see common.cuh).
+extern "C" int tsdg_gpu_phase_read(unsigned long long* out8, int reset) {
+    static unsigned long long host[1 << 16][8];
+    if (cudaMemcpyFromSymbol(host, tsdg_dev::g_phase, sizeof(host)) != cudaSuccess) return 2;
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+    for (int w = 0; w < (1 << 16); ++w)
+        for (int i = 0; i < 8; ++i) out8[i] += host[w][i];
+    if (reset) {
+        std::memset(host, 0, sizeof(host));
+        cudaMemcpyToSymbol(tsdg_dev::g_phase, host, sizeof(host));
+    }
+    return 0;
+}
+#endif
