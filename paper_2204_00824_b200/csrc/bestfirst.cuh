@@ -23,9 +23,8 @@
 //     state IS the next admission.  A C-push that evicts an id sitting later in
 //     the chunk (skipped because it was queued) revives that edge, exactly as the
 //     sequential loop would see it;
-//   * L2 prefetch (no shared memory or registers held): the rows of the next chunk
-//     while this one is processed, and the adjacency row + deg_cut entry of every
-//     admitted node (the likely next expansions).
+//   * optional L2 prefetch (off by default, measured neutral): the rows of the next
+//     chunk, and the adjacency row + deg_cut entry of every admitted node.
 #pragma once
 
 #include "../../include/tsdg_gpu.h"
@@ -56,7 +55,7 @@ struct BfArgs {
     uint32_t dch;           // staged dims per row per round (multiple of 8, <= 128)
     uint32_t slots;         // staged rows per gather round (1..32)
     uint32_t prefetch;      // bit 0: next-chunk rows (L2), bit 1: admitted adjacency (L2),
-                            // bit 2: speculative next-hop adjacency load (registers)
+                            // bit 3: disable batched admission (sequential replay only)
     // per-warp shared-memory carve (bytes)
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
         off_vsize, off_voldest, off_rid, off_rdist, off_bar;
@@ -259,6 +258,107 @@ __device__ __forceinline__ void r_push_smem(BfWarp& w, uint32_t& rn, uint32_t e,
     __syncwarp();
 }
 
+// Number of entries of a sorted 32-lane list (lane t holds entry t; padded with
+// (+inf, kInvalid) sentinels) that are strictly closer than (xd, xi).  Per-lane
+// binary search through shuffles with per-lane source lanes.
+__device__ __forceinline__ uint32_t count_closer32(float vd, uint32_t vi, float xd, uint32_t xi) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+        const float pd = __shfl_sync(kFull, vd, (int)(pos + step - 1));
+        const uint32_t pi = __shfl_sync(kFull, vi, (int)(pos + step - 1));
+        if (closer(pd, pi, xd, xi)) pos += step;
+    }
+    const float ld = __shfl_sync(kFull, vd, 31);
+    const uint32_t li = __shfl_sync(kFull, vi, 31);
+    if (pos == 31 && closer(ld, li, xd, xi)) pos = 32;
+    return pos;
+}
+
+// Batched admission of one chunk for k <= 31 (R in registers, lane i = entry i).
+//
+// The reference admits the chunk's candidates one by one in edge order with the
+// test dist < R.furthest().dist || |R| < k (bestfirst_search.cpp:91).  A rejected
+// candidate is never closer than the current k-th distance, so counting it in the
+// multiset does not move the k-th smallest distance; hence candidate j is admitted
+// iff fewer than k of {R} u {needed candidates before j} have distance <= dist_j.
+// The final R is the k smallest by (dist, id) of R u admitted (each push + pop of
+// the farthest keeps exactly that).  C's final content without a full segment is
+// order independent and no eviction happens.  Two cases make order matter and fall
+// back to the sequential replay (returns false, nothing modified): a needed id
+// already held by R (TopK::push is then a no-op) and a C segment that would overflow.
+__device__ __forceinline__ bool admit_batch_reg(BfWarp& w, uint32_t m, uint32_t k, RReg& rr,
+                                                uint32_t& rn, float& rfar, bool need, float dist,
+                                                uint32_t e, uint32_t& ctotal, uint32_t& evictions,
+                                                int lane) {
+    const float kInf = __int_as_float(0x7f800000);
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return true;
+    const float rdv = (uint32_t)lane < rn ? rr.d : kInf;
+    const uint32_t riv = (uint32_t)lane < rn ? rr.i : kInvalid;
+    bool dup = false;
+    for (uint32_t i = 0; i < rn; ++i) dup |= need && (__shfl_sync(kFull, riv, (int)i) == e);
+    if (__any_sync(kFull, dup)) return false;
+    // #R entries with distance <= dist (R sorted; padded with +inf)
+    uint32_t cnt = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+        const float v = __shfl_sync(kFull, rdv, (int)(cnt + step - 1));
+        if (v <= dist) cnt += step;
+    }
+    // + earlier needed candidates with distance <= dist
+    unsigned mm = nm & ((1u << lane) - 1u);
+    unsigned rest = nm;
+    while (rest) {
+        const int i = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const float di = __shfl_sync(kFull, dist, i);
+        if ((mm >> i) & 1u) cnt += (di <= dist) ? 1u : 0u;
+    }
+    const bool admit = need && cnt < k;
+    const unsigned am = __ballot_sync(kFull, admit);
+    if (am == 0) return true;
+    const uint32_t s = seg_of(e, m);
+    const unsigned same = __match_any_sync(kFull, admit ? s : 0xFFFFFFFFu) & am;
+    const bool over = admit && (w.csize[s] + __popc(same) > 32u);
+    if (__any_sync(kFull, over)) return false;
+    // R <- k smallest of R u A
+    float ad = admit ? dist : kInf;
+    uint32_t ai = admit ? e : kInvalid;
+    warp_sort32(ad, ai, lane);
+    const uint32_t na = __popc(am);
+    const uint32_t rank_r = (uint32_t)lane + count_closer32(ad, ai, rdv, riv);
+    const uint32_t rank_a = (uint32_t)lane + count_closer32(rdv, riv, ad, ai);
+    float* sd = w.cdist + m * kSegPitch;  // scratch row after C (carved by the host)
+    uint32_t* si = w.cid + m * kSegPitch;
+    __syncwarp();
+    if ((uint32_t)lane < rn && rank_r < k) {
+        sd[rank_r] = rdv;
+        si[rank_r] = riv;
+    }
+    if ((uint32_t)lane < na && rank_a < k) {
+        sd[rank_a] = ad;
+        si[rank_a] = ai;
+    }
+    __syncwarp();
+    rn = min(k, rn + na);
+    if ((uint32_t)lane < rn) {
+        rr.d = sd[lane];
+        rr.i = si[lane];
+    }
+    __syncwarp();
+    rfar = __shfl_sync(kFull, rr.d, (int)rn - 1);
+    // C pushes (no segment overflows: order independent, no evictions)
+    rest = am;
+    while (rest) {
+        const int p = __ffs(rest) - 1;
+        rest &= rest - 1;
+        c_push(w, m, __shfl_sync(kFull, e, p), __shfl_sync(kFull, dist, p), ctotal, evictions,
+               lane);
+    }
+    return true;
+}
+
 __device__ __forceinline__ void prefetch_rows(const BfArgs& a, bool want, uint32_t e) {
     if (want) {
         const char* p = reinterpret_cast<const char*>(a.vec + (size_t)e * a.ld);
@@ -293,7 +393,7 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
     const float kInf = __int_as_float(0x7f800000);
     const bool pf_rows = (a.prefetch & 1u) != 0;
     const bool pf_adj = (a.prefetch & 2u) != 0;
-    const bool spec = (a.prefetch & 4u) != 0;
+    const bool batch = (a.prefetch & 8u) == 0;  // batched admission (default on)
 
     for (;;) {
         uint32_t q = 0;
@@ -327,8 +427,6 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
         c_push(w, a.m, si, sd, ctotal, evictions, lane);
         float rfar = KREG ? __shfl_sync(kFull, rr.d, rn - 1) : w.rdist[rn - 1];
         PH_MARK(0)
-        // speculative next expansion (see below): its deg + first 64 adjacency entries
-        uint32_t spec_u = kInvalid, spec_deg = 0, spec_e0 = kInvalid, spec_e1 = kInvalid;
 
         while (ctotal > 0 && hops < a.hop_limit) {  // :73
             ++hops;
@@ -339,17 +437,9 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
             // issue the dependent loads first (unless the speculation already did), then
             // V.add while they fly
             const uint32_t* arow = a.adj + (size_t)u * a.R;
-            uint32_t deg, e_next, e_next2;
-            if (u == spec_u) {
-                deg = spec_deg;
-                e_next = spec_e0;
-                e_next2 = spec_e1;
-            } else {
-                deg = __ldg(a.degcut + u);
-                e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
-                e_next2 = (uint32_t)lane + 32 < a.R ? __ldg(arow + 32 + lane) : kInvalid;
-            }
-            spec_u = kInvalid;
+            const uint32_t deg = __ldg(a.degcut + u);
+            uint32_t e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
+            uint32_t e_next2 = (uint32_t)lane + 32 < a.R ? __ldg(arow + 32 + lane) : kInvalid;
             v_add(w, a.m, u, lane);
             examined += deg;
             PH_MARK(1)
@@ -360,8 +450,11 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
                 e_next = e_next2;
                 const uint32_t j2 = base + 64 + lane;
                 e_next2 = (base + 64 < deg && j2 < a.R) ? __ldg(arow + j2) : kInvalid;
-                const bool inV = valid && v_contains(w, a.m, e);
-                const bool inC = valid && !inV && c_contains(w, a.m, e);
+                // both scans unconditionally: independent LDS streams overlap
+                const bool sV = valid && v_contains(w, a.m, e);
+                const bool sC = valid && c_contains(w, a.m, e);
+                const bool inV = sV;
+                const bool inC = sC && !sV;
                 const bool need = valid && !inV && !inC;
                 if (pf_rows && base + 32 < deg) {
                     // next chunk: prefetch rows of edges not visited (V is fixed for
@@ -372,36 +465,12 @@ __global__ void __launch_bounds__(kBfWarps * 32) bf_kernel(const BfArgs a) {
                 PH_MARK(2)
                 float dist = gather_eval<METRIC, FAST, STAGE>(w.st, g, need, e, lane);
                 PH_RESET
-                if (spec && base + 32 >= deg) {
-                    // Last chunk of the hop: the next pop is C's minimum after these
-                    // admissions = closer of (current C head, best candidate passing the
-                    // admission test) in all but rare eviction / tie cases.  Issue its
-                    // deg_cut + adjacency loads now so they overlap the admission replay;
-                    // the next hop uses them only if it pops exactly that node.
-                    float cd = (need && (dist < rfar || rn < a.k)) ? dist : kInf;
-                    uint32_t ci = (need && (dist < rfar || rn < a.k)) ? e : kInvalid;
-                    for (uint32_t sg = lane; sg < a.m; sg += 32) {
-                        if (w.csize[sg] != 0) {
-                            const float hd = w.cdist[sg * kSegPitch];
-                            const uint32_t hi = w.cid[sg * kSegPitch];
-                            if (closer(hd, hi, cd, ci)) {
-                                cd = hd;
-                                ci = hi;
-                            }
-                        }
-                    }
-                    warp_argmin(cd, ci);
-                    spec_u = ci;
-                    if (ci != kInvalid) {
-                        const uint32_t* srow = a.adj + (size_t)ci * a.R;
-                        spec_deg = __ldg(a.degcut + ci);
-                        spec_e0 = (uint32_t)lane < a.R ? __ldg(srow + lane) : kInvalid;
-                        spec_e1 = (uint32_t)lane + 32 < a.R ? __ldg(srow + 32 + lane) : kInvalid;
-                    }
-                }
                 unsigned pending = __ballot_sync(kFull, need);
                 unsigned revivable = __ballot_sync(kFull, inC);
                 evals += __popc(pending);
+                if (KREG && batch &&
+                    admit_batch_reg(w, a.m, a.k, rr, rn, rfar, need, dist, e, ctotal, evictions, lane))
+                    pending = 0;
                 while (pending) {
                     const bool ok = ((pending >> lane) & 1u) && (dist < rfar || rn < a.k);
                     const unsigned adm = __ballot_sync(kFull, ok);

@@ -43,30 +43,6 @@ struct GrArgs {
     uint32_t warp_smem, off_query, off_stage, off_bar;
 };
 
-// compare-exchange keeping min (keep_min) or max of (d,id) vs partner's
-__device__ __forceinline__ void cx(float& d, uint32_t& id, float od, uint32_t oi, bool keep_min) {
-    const bool other_first = closer(od, oi, d, id);
-    if (keep_min == other_first) {
-        d = od;
-        id = oi;
-    }
-}
-
-// Ascending bitonic sort of 32 keys, one per lane.
-__device__ __forceinline__ void warp_sort32(float& d, uint32_t& id, int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const float od = __shfl_xor_sync(kFull, d, j);
-            const uint32_t oi = __shfl_xor_sync(kFull, id, j);
-            const bool up = (lane & k) == 0;
-            const bool lower = (lane & j) == 0;
-            cx(d, id, od, oi, lower == up);
-        }
-    }
-}
-
 // Ascending bitonic sort of 64 keys: (da,ia) is index lane, (db,ib) index 32+lane.
 __device__ __forceinline__ void warp_sort64(float& da, uint32_t& ia, float& db, uint32_t& ib,
                                             int lane) {

@@ -148,8 +148,8 @@ void fill_bf_layout(BfArgs& a) {
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
     a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
-    a.off_cid = c.take(a.m * kSegPitch * 4);
-    a.off_cdist = c.take(a.m * kSegPitch * 4);
+    a.off_cid = c.take((a.m + 1) * kSegPitch * 4);    // + one scratch row (batched admission)
+    a.off_cdist = c.take((a.m + 1) * kSegPitch * 4);
     a.off_csize = c.take(a.m * 4);
     a.off_vid = c.take(a.m * kSegPitch * 4);
     a.off_vsize = c.take(a.m * 4);
