@@ -297,7 +297,10 @@ __device__ __forceinline__ bool admit_batch_reg(BfWarp& w, uint32_t m, uint32_t 
     const float rdv = (uint32_t)lane < rn ? rr.d : kInf;
     const uint32_t riv = (uint32_t)lane < rn ? rr.i : kInvalid;
     bool dup = false;
-    for (uint32_t i = 0; i < rn; ++i) dup |= need && (__shfl_sync(kFull, riv, (int)i) == e);
+    for (uint32_t i = 0; i < rn; ++i) {
+        const uint32_t ri = __shfl_sync(kFull, riv, (int)i);  // every lane: no short-circuit
+        dup |= need && ri == e;
+    }
     if (__any_sync(kFull, dup)) return false;
     // #R entries with distance <= dist (R sorted; padded with +inf)
     uint32_t cnt = 0;
