@@ -38,6 +38,7 @@ struct Geom {
     const float* vec;
     uint32_t ld, d, dch;
     uint32_t slots;  // shared-memory row slots per warp (1..32)
+    uint32_t pitch;  // floats between slots (0: dch + 4, an odd number of 16-byte units)
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -120,6 +121,12 @@ __device__ __forceinline__ void row_quads(const float* srow, const float* sq, ui
             if (FAST) acc2 = acc4_fast<METRIC>(acc2, q2[i], r2[i]);
             else acc = acc4_exact2<METRIC>(acc, q2[i], r2[i]);
         }
+    } else if (q1 - q0 == 8) {
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) {
+            if (FAST) acc2 = acc4_fast<METRIC>(acc2, q2[q0 + i], r2[q0 + i]);
+            else acc = acc4_exact2<METRIC>(acc, q2[q0 + i], r2[q0 + i]);
+        }
     } else if (q1 - q0 == 16) {
 #pragma unroll
         for (uint32_t i = 0; i < 16; ++i) {
@@ -147,7 +154,7 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
     const unsigned nm = __ballot_sync(kFull, need);
     if (nm == 0) return kInf;
     PH_DECL
-    const uint32_t pitch = g.dch + 4;
+    const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
     const uint32_t cnt = __popc(nm);
     const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
     const float* row_src = g.vec + (size_t)(need ? e : 0) * g.ld;

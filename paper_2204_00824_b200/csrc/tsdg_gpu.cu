@@ -161,8 +161,10 @@ void fill_bf_layout(BfArgs& a) {
 }
 
 // Tuning knobs (environment, read per launch): TSDG_STAGE=tma (default)|ldgsts,
-// TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency, 4: speculative
-// next-hop adjacency; default 0: measured slower on C2, see profiles/),
+// TSDG_PREFETCH=<bits> (1: next-chunk rows, 2: admitted adjacency; default 0:
+// measured neutral-to-slower on C2, see profiles/),
+// TSDG_BATCH_MIN=<n> (batched admission when >= n candidates pass the bound; default
+// 0 = off: its fixed cost exceeded the sequential replay's on C2, 1.27 vs 1.16 ms),
 // TSDG_BF_WARPS=<warps per CTA> (default 1: finest shared-memory granularity),
 // TSDG_SLOTS=<staged rows per gather round> (default 16).
 int env_int(const char* name, int dflt) {
@@ -312,6 +314,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.dch = staging_dims(idx->ld);
     a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
     a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
+    a.batch_min = (uint32_t)std::max(0, env_int("TSDG_BATCH_MIN", 0));
     fill_bf_layout(a);
     const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
     const size_t smem = (size_t)a.warp_smem * wpc;

@@ -17,7 +17,8 @@ from paper_2204_00824_b200 import _native, datasets  # noqa: E402
 from paper_2204_00824_b200.search import BestFirstParams, GpuIndex, load_tsdg  # noqa: E402
 
 name = os.environ.get("SWEEP_DATASET", "c2_lowlid_1m")
-variants = [v.split(":") for v in sys.argv[1:]] or [["det", "ldgsts", "3"]]
+# each variant: mode[:ENV=VALUE[:ENV=VALUE...]]  e.g.  fast:TSDG_SLOTS=16:TSDG_BATCH_MIN=8
+variants = [v.split(":") for v in sys.argv[1:]] or [["fast"]]
 ks = [int(x) for x in os.environ.get("SWEEP_K", "16").split(",")]
 t = time.time()
 ds = datasets.load(name)
@@ -35,13 +36,9 @@ for k in ks:
     cc = torch.empty(nq, dtype=torch.int32, device=dev)
     stt = torch.empty((nq, 4), dtype=torch.int32, device=dev)
     for var in variants:
-        mode, stage, pf = var[:3]
-        wpc = var[3] if len(var) > 3 else "1"
-        slots = var[4] if len(var) > 4 else "32"
-        os.environ["TSDG_STAGE"] = stage
-        os.environ["TSDG_PREFETCH"] = pf
-        os.environ["TSDG_BF_WARPS"] = wpc
-        os.environ["TSDG_SLOTS"] = slots
+        mode, envs = var[0], dict(kv.split("=", 1) for kv in var[1:])
+        saved = {kk: os.environ.get(kk) for kk in envs}
+        os.environ.update(envs)
         m = _native.MODE_FAST if mode == "fast" else _native.MODE_DETERMINISTIC
 
         def step():
@@ -66,7 +63,12 @@ for k in ks:
         rec = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(), ds.gt, 10)
         ms = float(np.median(times))
         alg = 4 * ds.base.shape[1] * st[:, 1].sum() + 4 * st[:, 3].sum() + nq * (4 * ds.base.shape[1] + 8 * k)
-        print(json.dumps({"k": k, "mode": mode, "stage": stage, "prefetch": pf, "warps": wpc, "slots": slots, "ms": ms,
+        for kk, vv in saved.items():
+            if vv is None:
+                os.environ.pop(kk, None)
+            else:
+                os.environ[kk] = vv
+        print(json.dumps({"k": k, "mode": mode, "env": envs, "ms": ms,
                           "qps": nq / ms * 1e3, "recall10": rec, "alg_GBps": alg / ms / 1e6,
                           "evals_q": float(st[:, 1].mean()), "hops_q": float(st[:, 0].mean())}),
               flush=True)
