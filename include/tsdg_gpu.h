@@ -159,6 +159,34 @@ int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
                                  uint32_t shards, uint32_t nq, uint32_t k, uint32_t* d_out_ids,
                                  float* d_out_dists, uint32_t* d_out_counts, void* stream);
 
+/* ---- exact top-k scan ----------------------------
+ * Per query the k smallest (dist, id) pairs over every base row, distances bit-equal
+ * to the reference's kernel (sequential fp32, vectors.hpp:36-49), ties by id
+ * (common.hpp:22-25).  Output nq x k ascending, padded 0xFFFFFFFF / +inf.  GPU
+ * limit: k <= 384.
+ *
+ * tsdg_gpu_ground_truth replaces tsdg::ground_truth (bench.cpp:35-57; same checks:
+ * 1 <= k_gt <= n) and ref::exact_topk (reference.cpp:96-111); dists may be NULL.
+ * tsdg_gpu_index_ground_truth: the same over an index's resident vector store.
+ * tsdg_gpu_brute_force_knn replaces tsdg::brute_force_knn (knn_graph.cpp:64-86):
+ * the self pair is excluded, n < 2 and k < 1 are invalid, k > n-1 is clamped to n-1
+ * (warning on stderr, knn_graph.cpp:17-26) and returned in *k_eff; ids/dists are
+ * n x k_eff (the KnnGraph flat layout, knn_graph.hpp:15-28).
+ * tsdg_gpu_exact_topk_device: DEVICE pointers, row strides ld_* (multiples of 4
+ * floats), asynchronous on `stream`; exclude_self skips base row self_base + q for
+ * query q. */
+int tsdg_gpu_ground_truth(const float* base, uint32_t n, const float* queries, uint32_t nq,
+                          uint32_t d, uint32_t k_gt, int metric, int device, uint32_t* ids,
+                          float* dists);
+int tsdg_gpu_index_ground_truth(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                                uint32_t k_gt, uint32_t* ids, float* dists);
+int tsdg_gpu_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                             int device, uint32_t* ids, float* dists, uint32_t* k_eff);
+int tsdg_gpu_exact_topk_device(const float* d_base, uint32_t n, uint32_t ld_base,
+                               const float* d_queries, uint32_t nq, uint32_t ld_queries,
+                               uint32_t d, uint32_t k, int metric, int exclude_self,
+                               uint64_t self_base, uint32_t* d_ids, float* d_dists, void* stream);
+
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t tsdg_gpu_launch_count(void);
 

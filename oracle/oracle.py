@@ -284,6 +284,20 @@ class Oracle:
                                   ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids), _p(dists))
         return ids, dists
 
+    def brute_force_knn(self, base, k, metric=0):
+        """knn_graph.cpp:64-86 restated; k clamped to n-1 like clamp_k (:17-26)."""
+        b = np.ascontiguousarray(base, np.float32)
+        n = b.shape[0]
+        k = min(k, n - 1)
+        ids = np.empty((n, k), np.uint32)
+        dists = np.empty((n, k), np.float32)
+        rc = self.so.tsdg_o_brute_force_knn(_p(b), ctypes.c_uint32(n), ctypes.c_uint32(b.shape[1]),
+                                            ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids),
+                                            _p(dists))
+        if rc:
+            raise ValueError("brute_force_knn: invalid argument")
+        return ids, dists
+
 
 # ---------------------------------------------------------------- the reference itself
 def ref_available() -> bool:
@@ -426,6 +440,18 @@ class Ref:
                                           ctypes.c_uint32(q.shape[0]), ctypes.c_uint32(b.shape[1]),
                                           ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids), _p(dists)))
         return ids, dists
+
+    def brute_force_knn(self, base, k, metric=0):
+        b = np.ascontiguousarray(base, np.float32)
+        n = b.shape[0]
+        kk = max(1, min(k, n - 1))
+        ids = np.empty((n, kk), np.uint32)
+        dists = np.empty((n, kk), np.float32)
+        keff = ctypes.c_uint32()
+        self.check(self.so.ref_brute_force_knn(_p(b), ctypes.c_uint32(n), ctypes.c_uint32(b.shape[1]),
+                                               ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids),
+                                               _p(dists), ctypes.byref(keff)))
+        return ids[:, :keff.value], dists[:, :keff.value]
 
 
 class RefFixture:

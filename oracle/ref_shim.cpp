@@ -553,4 +553,18 @@ int ref_exact_topk(const float* base, std::uint32_t n, const float* queries,
     });
 }
 
+// tsdg::brute_force_knn (knn_graph.cpp:64-86), unmodified; k_eff = clamped k.
+int ref_brute_force_knn(const float* base, std::uint32_t n, std::uint32_t d, std::uint32_t k,
+                        int metric, std::uint32_t* ids_out, float* dists_out,
+                        std::uint32_t* k_eff) {
+    return guarded([&] {
+        const auto g = brute_force_knn(make_set(base, n, d), k, static_cast<Metric>(metric));
+        *k_eff = g.k;
+        for (std::size_t i = 0; i < g.flat.size(); ++i) {
+            ids_out[i] = g.flat[i].id;
+            dists_out[i] = g.flat[i].dist;
+        }
+    });
+}
+
 }  // extern "C"

@@ -568,3 +568,31 @@ int tsdg_o_exact_topk(const float* base, uint32_t n, const float* queries, uint3
     free(kept);
     return 0;
 }
+
+/* knn_graph.cpp:64-86 brute_force_knn (BoundedPool, knn_graph.cpp:28-60): for every
+ * node the k smallest (dist, id) over all other nodes; k already clamped by the
+ * caller (clamp_k, knn_graph.cpp:17-26).  Output n x k ascending. */
+int tsdg_o_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                           uint32_t* ids, float* dists) {
+    if (n < 2 || k < 1 || k > n - 1) return 1;
+    IdDist* kept = (IdDist*)malloc(sizeof(IdDist) * ((size_t)k + 1));
+    if (!kept) return 2;
+    for (uint32_t i = 0; i < n; ++i) {
+        uint32_t nk = 0;
+        for (uint32_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            IdDist e = {j, tsdg_o_distance(base + (size_t)i * d, base + (size_t)j * d, d, metric)};
+            if (nk == k && !closer(e, kept[nk - 1])) continue;
+            uint32_t pos = nk;
+            while (pos > 0 && closer(e, kept[pos - 1])) { kept[pos] = kept[pos - 1]; pos--; }
+            kept[pos] = e;
+            if (nk < k) nk++;
+        }
+        for (uint32_t t = 0; t < k; ++t) {
+            ids[(size_t)i * k + t] = kept[t].id;
+            dists[(size_t)i * k + t] = kept[t].dist;
+        }
+    }
+    free(kept);
+    return 0;
+}

@@ -78,6 +78,8 @@ int tsdg_o_topk_replay(uint32_t k, const uint8_t* ops, const uint32_t* ids,
                        uint32_t* final_ids, float* final_dists, uint32_t* final_n);
 int tsdg_o_exact_topk(const float* base, uint32_t n, const float* queries, uint32_t nq,
                       uint32_t d, uint32_t k, int metric, uint32_t* ids, float* dists);
+int tsdg_o_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                           uint32_t* ids, float* dists);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,11 @@ SIGNATURES = {
     "tsdg_gpu_greedy_once": (_I, [_VP, _VP, _U32, _VP, _U32, _U32, _VP, _VP, _VP]),
     "tsdg_gpu_merge_shards_device": (_I, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _VP, _VP, _VP,
                                           _VP]),
+    "tsdg_gpu_ground_truth": (_I, [_VP, _U32, _VP, _U32, _U32, _U32, _I, _I, _VP, _VP]),
+    "tsdg_gpu_index_ground_truth": (_I, [_VP, _VP, _U32, _U32, _VP, _VP]),
+    "tsdg_gpu_brute_force_knn": (_I, [_VP, _U32, _U32, _U32, _I, _I, _VP, _VP, _VP]),
+    "tsdg_gpu_exact_topk_device": (_I, [_VP, _U32, _U32, _VP, _U32, _U32, _U32, _U32, _I, _I,
+                                        _U64, _VP, _VP, _VP]),
 }
 
 _lib = None

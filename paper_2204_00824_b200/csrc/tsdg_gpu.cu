@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/tsdg_gpu.h"
+#include "exact_scan.cuh"
 #include "greedy_cluster.cuh"
 #include "unbounded.cuh"
 
@@ -547,6 +548,116 @@ void check_cosine_queries(const tsdg_gpu_index* idx, const float* queries, uint3
 
 }  // namespace
 
+namespace {
+
+// ---- exact top-k scan (ground truth / brute-force k-NN graph) ----------------
+constexpr uint32_t kScanMaxK = 384;
+// Candidate buffer per query: the next power of 2 >= k + one tile of rows.
+uint32_t scan_buffer(uint32_t k) {
+    uint32_t P = 1;
+    while (P < k + kScanBT) P <<= 1;
+    return P;
+}
+size_t scan_smem(uint32_t P) {
+    return (size_t)kScanDC * kScanQT * 8 + (size_t)kScanDC * kScanBPitch * 4 +
+           (size_t)kScanQT * P * 8 + kScanQT * 12;
+}
+
+void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const float* d_queries,
+                       uint32_t nq, uint32_t ld_q, uint32_t d, uint32_t k, int metric,
+                       int exclude_self, uint64_t self_base, uint32_t* d_ids, float* d_dists,
+                       cudaStream_t st) {
+    if (nq == 0) return;
+    if (k < 1 || k > kScanMaxK) fail(TSDG_EINVAL, "exact_topk: need 1 <= k <= 384");
+    if (d < 1 || ld_b % 4 || ld_q % 4 || ld_b < d || ld_q < d)
+        fail(TSDG_EINVAL, "exact_topk: row strides must be multiples of 4 floats and >= d");
+    if (metric < 0 || metric > 2) fail(TSDG_EINVAL, "invalid metric");
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    int sms = 148;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    ScanArgs a{};
+    a.base = d_base;
+    a.queries = d_queries;
+    a.n = n;
+    a.nq = nq;
+    a.d = d;
+    a.ld_b = ld_b;
+    a.ld_q = ld_q;
+    a.k = k;
+    a.P = scan_buffer(k);
+    a.exclude_self = exclude_self;
+    a.self_base = self_base;
+    a.keep = ~0ull;
+    const size_t smem = scan_smem(a.P);
+    void (*kern)(ScanArgs) = metric == 0 ? exact_scan_kernel<0>
+                             : metric == 1 ? exact_scan_kernel<1> : exact_scan_kernel<2>;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute(exact_scan)");
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kScanThreads, smem),
+               "occupancy(exact_scan)");
+    const uint32_t slots = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
+    const uint32_t qtiles = (nq + kScanQT - 1) / kScanQT;
+    // split the base rows so that the grid is >= ~4 waves; each split >= 8 tiles
+    uint32_t S = std::max<uint32_t>(1, (4 * slots + qtiles - 1) / qtiles);
+    S = std::min<uint32_t>(S, std::max<uint32_t>(1, n / (8 * kScanBT)));
+    S = std::min<uint32_t>(S, 64);
+    if (env_int("TSDG_SCAN_SPLITS", 0) > 0) S = (uint32_t)env_int("TSDG_SCAN_SPLITS", 0);
+    uint32_t rows = round_up((std::max<uint32_t>(n, 1) + S - 1) / S, kScanBT);
+    S = std::max<uint32_t>(1, (n + rows - 1) / rows);
+    a.rows_per_split = rows;
+    uint32_t* tids = d_ids;
+    float* tdist = d_dists;
+    if (S > 1) {
+        tids = dev_alloc<uint32_t>((size_t)S * nq * k, st);
+        tdist = dev_alloc<float>((size_t)S * nq * k, st);
+    }
+    a.out_ids = tids;
+    a.out_dists = tdist;
+    kern<<<dim3(qtiles, S), kScanThreads, smem, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "exact_scan_kernel launch");
+    if (S > 1) {
+        merge_splits_kernel<<<(nq + 7) / 8, 256, 0, st>>>(tids, tdist, S, nq, k, d_ids, d_dists);
+        g_launches++;
+        cuda_check(cudaGetLastError(), "merge_splits_kernel launch");
+        cudaFreeAsync(tids, st);
+        cudaFreeAsync(tdist, st);
+    }
+}
+
+// Host rows (n x d, dense) -> device rows padded to ld = round_up(d, 4), zero fill.
+float* upload_rows(const float* h, uint32_t n, uint32_t d, uint32_t ld, cudaStream_t st) {
+    float* p = dev_alloc<float>((size_t)std::max<uint32_t>(n, 1) * ld, st);
+    if (!n) return p;
+    if (ld == d) {
+        cuda_check(cudaMemcpyAsync(p, h, (size_t)n * d * 4, cudaMemcpyHostToDevice, st), "H2D rows");
+    } else {
+        cuda_check(cudaMemsetAsync(p, 0, (size_t)n * ld * 4, st), "memset rows");
+        cuda_check(cudaMemcpy2DAsync(p, ld * 4, h, d * 4, d * 4, n, cudaMemcpyHostToDevice, st),
+                   "H2D rows");
+    }
+    return p;
+}
+
+void scan_to_host(const float* d_base, uint32_t n, uint32_t ld, const float* d_queries, uint32_t nq,
+                  uint32_t d, uint32_t k, int metric, int exclude_self, uint32_t* ids,
+                  float* dists, cudaStream_t st) {
+    uint32_t* di = dev_alloc<uint32_t>((size_t)nq * k, st);
+    float* dd = dev_alloc<float>((size_t)nq * k, st);
+    launch_exact_topk(d_base, n, ld, d_queries, nq, ld, d, k, metric, exclude_self, 0, di, dd, st);
+    cuda_check(cudaMemcpyAsync(ids, di, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+    if (dists)
+        cuda_check(cudaMemcpyAsync(dists, dd, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st),
+                   "D2H dists");
+    cudaFreeAsync(di, st);
+    cudaFreeAsync(dd, st);
+    cuda_check(cudaStreamSynchronize(st), "exact_topk");
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* tsdg_gpu_last_error(void) { return g_err.c_str(); }
@@ -906,6 +1017,97 @@ int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
         g_launches++;
         cuda_check(cudaGetLastError(), "merge_shards_kernel launch");
         cudaFreeAsync(dbase, st);
+    });
+}
+
+
+// ---- exact top-k: ground truth / brute-force k-NN graph -------------------------
+int tsdg_gpu_exact_topk_device(const float* d_base, uint32_t n, uint32_t ld_base,
+                               const float* d_queries, uint32_t nq, uint32_t ld_queries,
+                               uint32_t d, uint32_t k, int metric, int exclude_self,
+                               uint64_t self_base, uint32_t* d_ids, float* d_dists, void* stream) {
+    return guarded([&] {
+        if ((nq && (!d_queries || !d_ids || !d_dists)) || (n && !d_base))
+            fail(TSDG_EINVAL, "exact_topk: null pointer");
+        launch_exact_topk(d_base, n, ld_base, d_queries, nq, ld_queries, d, k, metric, exclude_self,
+                          self_base, d_ids, d_dists, (cudaStream_t)stream);
+    });
+}
+
+int tsdg_gpu_ground_truth(const float* base, uint32_t n, const float* queries, uint32_t nq,
+                          uint32_t d, uint32_t k_gt, int metric, int device, uint32_t* ids,
+                          float* dists) {
+    return guarded([&] {
+        // bench.cpp:38-41
+        if (k_gt < 1 || k_gt > n) fail(TSDG_EINVAL, "ground_truth: need 1 <= K_gt <= n");
+        if (d < 1) fail(TSDG_EINVAL, "ground_truth: dim mismatch");
+        if (!base || (nq && (!queries || !ids))) fail(TSDG_EINVAL, "ground_truth: null pointer");
+        DeviceGuard dg(device);
+        cudaStream_t st;
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        const uint32_t ld = round_up(d, 4);
+        float* db = upload_rows(base, n, d, ld, st);
+        float* dq = upload_rows(queries, nq, d, ld, st);
+        try {
+            if (nq) scan_to_host(db, n, ld, dq, nq, d, k_gt, metric, 0, ids, dists, st);
+        } catch (...) {
+            cudaFreeAsync(db, st);
+            cudaFreeAsync(dq, st);
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaFreeAsync(db, st);
+        cudaFreeAsync(dq, st);
+        cuda_check(cudaStreamSynchronize(st), "ground_truth");
+        cudaStreamDestroy(st);
+    });
+}
+
+int tsdg_gpu_index_ground_truth(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
+                                uint32_t k_gt, uint32_t* ids, float* dists) {
+    return guarded([&] {
+        if (!idx) fail(TSDG_EINVAL, "ground_truth: null index");
+        if (k_gt < 1 || k_gt > idx->n) fail(TSDG_EINVAL, "ground_truth: need 1 <= K_gt <= n");
+        if (nq && (!queries || !ids)) fail(TSDG_EINVAL, "ground_truth: null pointer");
+        std::lock_guard<std::mutex> lk(idx->mu);
+        DeviceGuard dg(idx->device);
+        cudaStream_t st = idx->stream;
+        float* dq = upload_rows(queries, nq, idx->d, idx->ld, st);
+        if (nq) scan_to_host(idx->vec, idx->n, idx->ld, dq, nq, idx->d, k_gt, idx->metric, 0, ids,
+                             dists, st);
+        cudaFreeAsync(dq, st);
+        cuda_check(cudaStreamSynchronize(st), "ground_truth");
+    });
+}
+
+int tsdg_gpu_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                             int device, uint32_t* ids, float* dists, uint32_t* k_eff) {
+    return guarded([&] {
+        // knn_graph.cpp:17-26 (clamp_k)
+        if (n < 2) fail(TSDG_EINVAL, "brute_force_knn: need at least 2 vectors");
+        if (k < 1) fail(TSDG_EINVAL, "brute_force_knn: k must be >= 1");
+        if (k > n - 1) {
+            std::fprintf(stderr, "brute_force_knn: k=%u clamped to n-1=%u\n", k, n - 1);
+            k = n - 1;
+        }
+        if (k_eff) *k_eff = k;
+        if (d < 1) fail(TSDG_EINVAL, "brute_force_knn: d must be >= 1");
+        if (!base || !ids) fail(TSDG_EINVAL, "brute_force_knn: null pointer");
+        DeviceGuard dg(device);
+        cudaStream_t st;
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        const uint32_t ld = round_up(d, 4);
+        float* db = upload_rows(base, n, d, ld, st);
+        try {
+            scan_to_host(db, n, ld, db, n, d, k, metric, 1, ids, dists, st);
+        } catch (...) {
+            cudaFreeAsync(db, st);
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaFreeAsync(db, st);
+        cuda_check(cudaStreamSynchronize(st), "brute_force_knn");
+        cudaStreamDestroy(st);
     });
 }
 

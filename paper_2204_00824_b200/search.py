@@ -10,6 +10,9 @@ Reference interface (paper_2204_00824, /root/reference/proj/include/tsdg):
   small_batch_search     greedy_search.hpp:55-60      -> small_batch_search / GpuIndex
   small_batch_search_one greedy_search.hpp:49-52      -> small_batch_search_one
   greedy_search_once     greedy_search.hpp:43-45      -> greedy_search_once
+  ground_truth           bench.hpp (bench.cpp:35-57)  -> ground_truth / GpuIndex.ground_truth
+  exact_topk             reference.hpp (reference.cpp:96-111) -> exact_topk
+  brute_force_knn        knn_graph.hpp:32             -> brute_force_knn
 Same field names, defaults, argument meaning and exception types
 (std::invalid_argument -> InvalidArgument(ValueError)); results come back as the
 reference's list-of-id-lists, and the extended calls also return fp32 distances
@@ -173,6 +176,15 @@ class GpuIndex:
     def handle(self):
         return self._h
 
+    def ground_truth(self, queries, k_gt: int) -> GroundTruth:
+        """Exact top-k_gt over the resident vector store (tsdg::ground_truth)."""
+        q = _f32rows(queries, self.d)
+        nq = q.shape[0]
+        ids = np.empty((nq, max(k_gt, 1)), np.uint32)
+        dists = np.empty((nq, max(k_gt, 1)), np.float32)
+        check(lib().tsdg_gpu_index_ground_truth(self._h, _p(q), nq, int(k_gt), _p(ids), _p(dists)))
+        return GroundTruth(int(k_gt), ids, dists)
+
     def deg_cut(self, lambda_cut: int) -> np.ndarray:
         out = np.empty(self.n, np.uint32)
         check(lib().tsdg_gpu_deg_cut(self._h, lambda_cut, _p(out)))
@@ -262,6 +274,57 @@ class GpuIndex:
             ctypes.c_void_p(stream or None)))
 
 
+@dataclass
+class GroundTruth:
+    """tsdg::GroundTruth (bench.hpp): k ids per query, plus the fp32 distances."""
+    k: int
+    ids: np.ndarray    # nq x k u32
+    dists: np.ndarray  # nq x k f32
+
+
+@dataclass
+class KnnGraph:
+    """tsdg::KnnGraph (knn_graph.hpp:15-28): n x k neighbours ascending by (dist, id)."""
+    n: int
+    k: int
+    ids: np.ndarray    # n x k u32
+    dists: np.ndarray  # n x k f32
+
+
+def ground_truth(base, queries, k_gt: int, metric: int = 0, device: int = 0) -> GroundTruth:
+    """tsdg::ground_truth (bench.cpp:35-57) on the GPU: exact top-k_gt by (dist, id)."""
+    b = _f32rows(base)
+    q = _f32rows(queries)
+    if q.shape[1] != b.shape[1]:
+        raise InvalidArgument("ground_truth: dim mismatch")
+    nq = q.shape[0]
+    ids = np.empty((nq, max(k_gt, 1)), np.uint32)
+    dists = np.empty((nq, max(k_gt, 1)), np.float32)
+    check(lib().tsdg_gpu_ground_truth(_p(b), b.shape[0], _p(q), nq, b.shape[1], int(k_gt),
+                                      int(metric), device, _p(ids), _p(dists)))
+    return GroundTruth(int(k_gt), ids, dists)
+
+
+def exact_topk(base, queries, k: int, metric: int = 0, device: int = 0):
+    """ref::exact_topk (reference.cpp:96-111): (ids, dists), nq x k."""
+    g = ground_truth(base, queries, k, metric, device)
+    return g.ids, g.dists
+
+
+def brute_force_knn(base, k: int, metric: int = 0, device: int = 0) -> KnnGraph:
+    """tsdg::brute_force_knn (knn_graph.cpp:64-86) on the GPU: exact k-NN graph, self
+    excluded, k clamped to n-1 (warning on stderr), same (dist, id) order."""
+    b = _f32rows(base)
+    n = b.shape[0]
+    kk = max(1, min(int(k), max(n - 1, 1)))
+    ids = np.empty((n, kk), np.uint32)
+    dists = np.empty((n, kk), np.float32)
+    keff = ctypes.c_uint32(0)
+    check(lib().tsdg_gpu_brute_force_knn(_p(b), n, b.shape[1], int(k), int(metric), device,
+                                         _p(ids), _p(dists), ctypes.byref(keff)))
+    return KnnGraph(n, int(keff.value), ids, dists)
+
+
 def merge_shards_device(ids_ptr: int, dists_ptr: int, counts_ptr: int, shard_base, shards: int,
                         nq: int, k: int, out_ids_ptr: int, out_dists_ptr: int,
                         out_counts_ptr: int, stream: int = 0) -> None:
@@ -317,4 +380,5 @@ def small_batch_search_one(graph, base, query, k: int, params: GreedyParams,
 __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "TsdgGraph",
            "GpuIndex", "load_tsdg", "large_batch_search", "bestfirst_search",
            "small_batch_search", "small_batch_search_one", "merge_shards_device",
+           "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]

@@ -1,0 +1,105 @@
+"""Exact top-k scan on full-size inputs (development / evidence tool; one GPU).
+
+  * ground truth at C2 (10K x 1M x 128, k=100) and C4 (10K x 1M x 960) through the
+    index-resident form, checked id-for-id against the reference's ground_truth
+    output stored in data/<name>/gt.u32 (tools/make_dataset.py);
+  * brute-force k-NN graph (k=100) of the C1 base (100K x 128).
+
+Prints one JSON line per case: seconds (CUDA events around the device call), pair
+distances per second and the fp32-pipe roofline (3 flops per pair-dim: sub, mul, add
+— no FMA, the reference's rounding)."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2204_00824_b200 import _native, datasets  # noqa: E402
+
+FP32_PEAK = 148 * 128 * 2 * 1.965e9  # packed f32x2: 2 flops / lane / cycle (~74.4 TFLOP/s)
+
+
+def timed(fn, reps=2):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return min(ts)
+
+
+def gt_case(name, k=100):
+    if not datasets.available(name):
+        return {"case": f"ground_truth {name}", "unavailable": "dataset missing"}
+    import ctypes
+
+    from paper_2204_00824_b200.search import ground_truth
+    ds = datasets.load(name)
+    n, d = ds.base.shape
+    nq = ds.queries.shape[0]
+    # host-API form (upload + scan + download), checked against the reference's GT
+    t0 = time.perf_counter()
+    r = ground_truth(ds.base, ds.queries, k)
+    host_s = time.perf_counter() - t0
+    same = bool(np.array_equal(r.ids[:, :ds.gt.shape[1]], ds.gt[:, :k]))
+    out = {"case": f"ground_truth {name}", "nq": nq, "n": n, "d": d, "k": k,
+           "ids_equal_reference_gt": same, "host_call_s": host_s}
+    if d % 4 == 0:  # device-resident form (rows already 16-byte strided)
+        db = torch.from_numpy(ds.base).cuda()
+        dq = torch.from_numpy(ds.queries).cuda()
+        ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        dd = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        L = _native.lib()
+
+        def call():
+            _native.check(L.tsdg_gpu_exact_topk_device(
+                ctypes.c_void_p(db.data_ptr()), n, d, ctypes.c_void_p(dq.data_ptr()), nq, d, d, k,
+                0, 0, 0, ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(dd.data_ptr()),
+                ctypes.c_void_p(st)))
+
+        sec = timed(call)
+        flops = 3.0 * nq * n * d
+        out.update({"device_s": sec, "pairs_per_s": nq * n / sec,
+                    "fp32_TFLOPs": flops / sec / 1e12, "fp32_frac": flops / sec / FP32_PEAK})
+    return out
+
+
+def knn_case(name="c1_lowlid_100k", k=100):
+    if not datasets.available(name):
+        return {"case": f"brute_force_knn {name}", "unavailable": "dataset missing"}
+    ds = datasets.load(name)
+    from paper_2204_00824_b200.search import brute_force_knn
+    n, d = ds.base.shape
+    t0 = time.perf_counter()
+    kg = brute_force_knn(ds.base, k)
+    sec = time.perf_counter() - t0
+    # spot-check 50 nodes against the oracle (exact top-k over all other rows)
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    rows = np.arange(0, n, n // 50)[:50]
+    ok = True
+    for r in rows:
+        wi, _ = orc.exact_topk(ds.base, ds.base[r:r + 1], k + 1)
+        want = [x for x in wi[0] if x != r][:k]
+        ok &= bool(np.array_equal(kg.ids[r], np.array(want, np.uint32)))
+    flops = 3.0 * n * n * d
+    return {"case": f"brute_force_knn {name}", "n": n, "d": d, "k": kg.k,
+            "host_call_s": sec, "fp32_TFLOPs_incl_copies": flops / sec / 1e12,
+            "oracle_spot_check_50_nodes": ok}
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:] or ["c2_lowlid_1m", "c4_lowlid_1m_960", "knn"]:
+        print(json.dumps(knn_case() if name == "knn" else gt_case(name)), flush=True)
