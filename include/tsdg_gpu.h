@@ -187,6 +187,32 @@ int tsdg_gpu_exact_topk_device(const float* d_base, uint32_t n, uint32_t ld_base
                                uint32_t d, uint32_t k, int metric, int exclude_self,
                                uint64_t self_base, uint32_t* d_ids, float* d_dists, void* stream);
 
+/* ---- GPU two-stage diversification ------------------------
+ * Replaces tsdg::build (diversify.cpp:152-209): stage 1 relaxed GD per node
+ * (:44-69), reverse edges with dedup and the dist_matches re-check (:71-124), stage
+ * 2 lambda counts with the lambda0 filter, (lambda, dist, target) order and the
+ * max_degree cap (:126-150).  Given the same KnnGraph (knn_ids / knn_dists: n x k,
+ * rows ascending by (dist, id) as brute_force_knn / nn_descent produce them) the
+ * result equals the reference's TsdgGraph edge for edge, fp32 distances included.
+ * Errors as the reference: alpha < 1 and unsorted candidate rows are invalid
+ * arguments (diversify.cpp:48-53,157), a target >= n too (add_reverse_edges throws
+ * std::out_of_range there).  GPU limit: k <= 128.  stats4 (nullable) = BuildStats
+ * {input_edges, stage1_edges, augmented_edges, final_edges} (diversify.hpp:39-44).
+ * The graph lives on the host: tsdg_gpu_graph_copy fills CSR arrays sized by
+ * tsdg_gpu_graph_info (offsets n+1, the rest num_edges); tsdg_gpu_graph_save writes
+ * the reference's file format (save_tsdg, diversify.cpp:252-272). */
+typedef struct tsdg_gpu_graph tsdg_gpu_graph;
+int tsdg_gpu_build(const float* base, uint32_t n, uint32_t d, const uint32_t* knn_ids,
+                   const float* knn_dists, uint32_t k, float alpha, uint16_t lambda0,
+                   uint32_t max_degree, int metric, int device, tsdg_gpu_graph** out,
+                   uint64_t* stats4);
+int tsdg_gpu_graph_info(const tsdg_gpu_graph* g, uint64_t* n, uint64_t* num_edges,
+                        uint32_t* max_degree);
+int tsdg_gpu_graph_copy(const tsdg_gpu_graph* g, uint64_t* offsets, uint32_t* targets,
+                        uint16_t* lambdas, float* dists);
+int tsdg_gpu_graph_save(const tsdg_gpu_graph* g, const char* path);
+int tsdg_gpu_graph_destroy(tsdg_gpu_graph* g);
+
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t tsdg_gpu_launch_count(void);
 

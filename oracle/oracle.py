@@ -441,6 +441,33 @@ class Ref:
                                           ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids), _p(dists)))
         return ids, dists
 
+    def nn_descent(self, base, k, iterations, sample_rate, seed, metric=0):
+        b = np.ascontiguousarray(base, np.float32)
+        n = b.shape[0]
+        kk = max(1, min(k, n - 1))
+        ids = np.empty((n, kk), np.uint32)
+        dists = np.empty((n, kk), np.float32)
+        keff = ctypes.c_uint32()
+        self.check(self.so.ref_nn_descent(_p(b), ctypes.c_uint32(n), ctypes.c_uint32(b.shape[1]),
+                                          ctypes.c_int(metric), ctypes.c_uint32(k),
+                                          ctypes.c_uint32(iterations), ctypes.c_double(sample_rate),
+                                          ctypes.c_uint64(seed), _p(ids), _p(dists),
+                                          ctypes.byref(keff)))
+        return ids[:, :keff.value], dists[:, :keff.value]
+
+    def build_from_knn(self, base, knn_ids, knn_dists, path, alpha=1.2, lambda0=9, max_degree=0,
+                       metric=0):
+        b = np.ascontiguousarray(base, np.float32)
+        ki = np.ascontiguousarray(knn_ids, np.uint32)
+        kd = np.ascontiguousarray(knn_dists, np.float32)
+        stats = (ctypes.c_uint64 * 4)()
+        self.check(self.so.ref_build_from_knn(_p(b), ctypes.c_uint32(b.shape[0]),
+                                              ctypes.c_uint32(b.shape[1]), ctypes.c_int(metric),
+                                              _p(ki), _p(kd), ctypes.c_uint32(ki.shape[1]),
+                                              ctypes.c_float(alpha), ctypes.c_uint32(lambda0),
+                                              ctypes.c_uint32(max_degree), str(path).encode(), stats))
+        return list(stats)
+
     def brute_force_knn(self, base, k, metric=0):
         b = np.ascontiguousarray(base, np.float32)
         n = b.shape[0]

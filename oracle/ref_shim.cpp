@@ -185,6 +185,49 @@ int ref_build_tsdg(const float* base, std::uint32_t n, std::uint32_t d, int metr
     });
 }
 
+// tsdg::nn_descent (knn_graph.cpp:141-251) rows: n x k_eff (id, dist).
+int ref_nn_descent(const float* base, std::uint32_t n, std::uint32_t d, int metric,
+                   std::uint32_t k, std::uint32_t iterations, double sample_rate,
+                   std::uint64_t seed, std::uint32_t* ids_out, float* dists_out,
+                   std::uint32_t* k_eff) {
+    return guarded([&] {
+        const auto g = nn_descent(make_set(base, n, d), k, static_cast<Metric>(metric),
+                                  iterations, sample_rate, seed);
+        *k_eff = g.k;
+        for (std::size_t i = 0; i < g.flat.size(); ++i) {
+            ids_out[i] = g.flat[i].id;
+            dists_out[i] = g.flat[i].dist;
+        }
+    });
+}
+
+// tsdg::build (diversify.cpp:152-209) from an explicit KnnGraph; saved with save_tsdg.
+int ref_build_from_knn(const float* base, std::uint32_t n, std::uint32_t d, int metric,
+                       const std::uint32_t* knn_ids, const float* knn_dists, std::uint32_t k,
+                       float alpha, std::uint32_t lambda0, std::uint32_t max_degree,
+                       const char* path, std::uint64_t* stats4) {
+    return guarded([&] {
+        KnnGraph knn;
+        knn.n = n;
+        knn.k = k;
+        knn.flat.resize(static_cast<std::size_t>(n) * k);
+        for (std::size_t i = 0; i < knn.flat.size(); ++i) knn.flat[i] = {knn_ids[i], knn_dists[i]};
+        DiversifyParams p;
+        p.alpha = alpha;
+        p.lambda0 = static_cast<std::uint16_t>(lambda0);
+        p.max_degree = max_degree;
+        BuildStats bs;
+        const TsdgGraph g = build(make_set(base, n, d), knn, p, static_cast<Metric>(metric), &bs);
+        save_tsdg(g, path);
+        if (stats4) {
+            stats4[0] = bs.input_edges;
+            stats4[1] = bs.stage1_edges;
+            stats4[2] = bs.augmented_edges;
+            stats4[3] = bs.final_edges;
+        }
+    });
+}
+
 // Saves an explicit CSR adjacency through tsdg_from_adjacency + save_tsdg
 // (diversify.cpp:211-272); validates ordering exactly like the reference.
 int ref_save_csr(std::uint32_t n, int metric, std::uint32_t k, float alpha,

@@ -66,6 +66,12 @@ SIGNATURES = {
     "tsdg_gpu_brute_force_knn": (_I, [_VP, _U32, _U32, _U32, _I, _I, _VP, _VP, _VP]),
     "tsdg_gpu_exact_topk_device": (_I, [_VP, _U32, _U32, _VP, _U32, _U32, _U32, _U32, _I, _I,
                                         _U64, _VP, _VP, _VP]),
+    "tsdg_gpu_build": (_I, [_VP, _U32, _U32, _VP, _VP, _U32, _F, ctypes.c_uint16, _U32, _I, _I,
+                            _VP, _VP]),
+    "tsdg_gpu_graph_info": (_I, [_VP, _VP, _VP, _VP]),
+    "tsdg_gpu_graph_copy": (_I, [_VP, _VP, _VP, _VP, _VP]),
+    "tsdg_gpu_graph_save": (_I, [_VP, ctypes.c_char_p]),
+    "tsdg_gpu_graph_destroy": (_I, [_VP]),
 }
 
 _lib = None

@@ -20,6 +20,9 @@
 #include <vector>
 
 #include "../../include/tsdg_gpu.h"
+#include <cub/device/device_scan.cuh>
+
+#include "diversify.cuh"
 #include "exact_scan.cuh"
 #include "greedy_cluster.cuh"
 #include "unbounded.cuh"
@@ -82,6 +85,18 @@ T* dev_alloc(size_t count, cudaStream_t st) {
 }  // namespace
 
 void tsdg_set_error(const std::string& msg) { g_err = msg; }
+
+// Host-side TSDG produced by tsdg_gpu_build (the reference's TsdgGraph fields).
+struct tsdg_gpu_graph {
+    uint32_t n = 0, k = 0;
+    int metric = 0;
+    float alpha = 1.2f;
+    uint16_t lambda0 = 9;
+    std::vector<uint64_t> offsets;
+    std::vector<uint32_t> targets;
+    std::vector<uint16_t> lambdas;
+    std::vector<float> dists;
+};
 
 struct tsdg_gpu_index {
     int device = 0;
@@ -656,6 +671,189 @@ void scan_to_host(const float* d_base, uint32_t n, uint32_t ld, const float* d_q
     cuda_check(cudaStreamSynchronize(st), "exact_topk");
 }
 
+// ---- GPU two-stage diversification (diversify.cuh) ------------------------------
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t st;
+    DevBuf(size_t n, cudaStream_t s) : st(s) { p = dev_alloc<T>(n, s); }
+    ~DevBuf() { cudaFreeAsync(p, st); }
+    DevBuf(const DevBuf&) = delete;
+};
+
+__global__ void div_total_kernel(const uint32_t* a, const uint32_t* b, uint32_t n,
+                                 unsigned long long* out) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) out[u + 1] = (unsigned long long)a[u] + (b ? b[u] : 0u);
+    if (u == 0) out[0] = 0;
+}
+__global__ void div_gather_kernel(const unsigned long long* src_off, const unsigned long long* dst_off,
+                                  const uint32_t* cnt, uint32_t n, const uint32_t* ids,
+                                  const uint16_t* lam, const float* dists, uint32_t* o_ids,
+                                  uint16_t* o_lam, float* o_dists) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (u >= n) return;
+    for (uint32_t j = lane; j < cnt[u]; j += 32) {
+        o_ids[dst_off[u] + j] = ids[src_off[u] + j];
+        o_lam[dst_off[u] + j] = lam[src_off[u] + j];
+        o_dists[dst_off[u] + j] = dists[src_off[u] + j];
+    }
+}
+
+// offsets[0..n] = prefix sums of a[u] (+ b[u]); returns the total.
+unsigned long long div_prefix(const uint32_t* a, const uint32_t* b, uint32_t n,
+                              unsigned long long* off, cudaStream_t st) {
+    div_total_kernel<<<(std::max<uint32_t>(n, 1) + 255) / 256, 256, 0, st>>>(a, b, n, off);
+    g_launches++;
+    size_t tmp = 0;
+    cuda_check(cub::DeviceScan::InclusiveSum(nullptr, tmp, off + 1, off + 1, (int)n, st), "cub scan");
+    DevBuf<char> t(tmp, st);
+    cuda_check(cub::DeviceScan::InclusiveSum(t.p, tmp, off + 1, off + 1, (int)n, st), "cub scan");
+    unsigned long long total = 0;
+    cuda_check(cudaMemcpyAsync(&total, off + n, 8, cudaMemcpyDeviceToHost, st), "D2H total");
+    cuda_check(cudaStreamSynchronize(st), "prefix");
+    return total;
+}
+
+void gpu_build(const float* base, uint32_t n, uint32_t d, const uint32_t* knn_ids,
+               const float* knn_dists, uint32_t k, float alpha, uint16_t lambda0,
+               uint32_t max_degree, int metric, tsdg_gpu_graph& g, uint64_t* stats,
+               cudaStream_t st) {
+    const uint32_t ld = round_up(d, 4);
+    float* vec = upload_rows(base, n, d, ld, st);
+    DevBuf<float> vec_keep(0, st);
+    std::swap(vec_keep.p, vec);
+    DivArgs a{};
+    a.vec = vec_keep.p;
+    a.n = n;
+    a.d = d;
+    a.ld = ld;
+    a.metric = metric;
+    a.keep = ~0ull;
+    a.k = k;
+    a.alpha = alpha;
+    a.lambda0 = lambda0;
+    a.max_degree = max_degree;
+    const size_t nk = (size_t)n * k;
+    DevBuf<uint32_t> kid(nk, st), s1i(nk, st), s1c(n, st), rc(n, st), cur(n, st), acnt(n, st),
+        ocnt(n, st);
+    DevBuf<float> kd(nk, st), s1d(nk, st);
+    DevBuf<int> err(1, st);
+    DevBuf<unsigned long long> aoff(n + 1, st), foff(n + 1, st);
+    cuda_check(cudaMemcpyAsync(kid.p, knn_ids, nk * 4, cudaMemcpyHostToDevice, st), "H2D knn");
+    cuda_check(cudaMemcpyAsync(kd.p, knn_dists, nk * 4, cudaMemcpyHostToDevice, st), "H2D knn");
+    cuda_check(cudaMemsetAsync(err.p, 0, 4, st), "memset");
+    cuda_check(cudaMemsetAsync(rc.p, 0, (size_t)n * 4, st), "memset");
+    cuda_check(cudaMemsetAsync(cur.p, 0, (size_t)n * 4, st), "memset");
+    a.knn_ids = kid.p;
+    a.knn_dists = kd.p;
+    a.s1_ids = s1i.p;
+    a.s1_dists = s1d.p;
+    a.s1_cnt = s1c.p;
+    a.err = err.p;
+    auto s1 = metric == 0 ? div_stage1_kernel<0> : metric == 1 ? div_stage1_kernel<1> : div_stage1_kernel<2>;
+    s1<<<n, kDivThreads, 0, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "div_stage1_kernel launch");
+    int herr = 0;
+    cuda_check(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st), "D2H err");
+    cuda_check(cudaStreamSynchronize(st), "div_stage1_kernel");
+    if (herr & 1) fail(TSDG_EINVAL, "stage1_relaxed_gd: candidates must be sorted ascending by distance");
+    if (herr & 2) fail(TSDG_EINVAL, "add_reverse_edges: target out of range");
+    const unsigned blocks_nk = (unsigned)((nk + 255) / 256);
+    div_rev_count_kernel<<<blocks_nk, 256, 0, st>>>(a, rc.p);
+    g_launches++;
+    const unsigned long long s1_edges = div_prefix(s1c.p, nullptr, n, foff.p, st);  // stage-1 count
+    const unsigned long long total = div_prefix(s1c.p, rc.p, n, aoff.p, st);
+    DevBuf<uint32_t> aid(total, st), tid_(total, st), tcnt(total, st), oid(total, st);
+    DevBuf<float> adist(total, st), tdist(total, st), odist(total, st);
+    DevBuf<uint16_t> olam(total, st);
+    a.aug_off = aoff.p;
+    a.aug_ids = aid.p;
+    a.aug_dists = adist.p;
+    a.aug_cnt = acnt.p;
+    a.tmp_ids = tid_.p;
+    a.tmp_dists = tdist.p;
+    a.tmp_cnt = tcnt.p;
+    a.out_ids = oid.p;
+    a.out_lambda = olam.p;
+    a.out_dists = odist.p;
+    a.out_cnt = ocnt.p;
+    div_fill_kernel<<<blocks_nk, 256, 0, st>>>(a, cur.p);
+    g_launches++;
+    div_dedup_kernel<<<(n + 7) / 8, 256, 0, st>>>(a);
+    g_launches++;
+    auto s2 = metric == 0 ? div_stage2_kernel<0> : metric == 1 ? div_stage2_kernel<1> : div_stage2_kernel<2>;
+    s2<<<n, kDivThreads, 0, st>>>(a);
+    g_launches++;
+    cuda_check(cudaGetLastError(), "div_stage2_kernel launch");
+    const unsigned long long aug_edges = div_prefix(acnt.p, nullptr, n, foff.p, st);
+    const unsigned long long fin = div_prefix(ocnt.p, nullptr, n, foff.p, st);
+    DevBuf<uint32_t> fid(fin, st);
+    DevBuf<uint16_t> flam(fin, st);
+    DevBuf<float> fdist(fin, st);
+    div_gather_kernel<<<(n + 7) / 8, 256, 0, st>>>(aoff.p, foff.p, ocnt.p, n, oid.p, olam.p, odist.p,
+                                                   fid.p, flam.p, fdist.p);
+    g_launches++;
+    g.offsets.resize((size_t)n + 1);
+    g.targets.resize(fin);
+    g.lambdas.resize(fin);
+    g.dists.resize(fin);
+    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+    cuda_check(cudaMemcpyAsync(g.offsets.data(), foff.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    if (fin) {
+        cuda_check(cudaMemcpyAsync(g.targets.data(), fid.p, fin * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(g.lambdas.data(), flam.p, fin * 2, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(g.dists.data(), fdist.p, fin * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    cuda_check(cudaStreamSynchronize(st), "gpu_build");
+    if (stats) {
+        stats[0] = (uint64_t)n * k;
+        stats[1] = s1_edges;
+        stats[2] = aug_edges;
+        stats[3] = fin;
+    }
+}
+
+void write_tsdg_file(const tsdg_gpu_graph& g, const char* path) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(TSDG_ERUNTIME, std::string(path) + ": cannot open for writing");
+    std::vector<unsigned char> buf;
+    auto put = [&](const void* p, size_t nb) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        buf.insert(buf.end(), c, c + nb);
+    };
+    const uint32_t version = 1;
+    const uint64_t n64 = g.n;
+    const uint8_t metric = (uint8_t)g.metric;
+    put("TSDG", 4);  // little-endian host (x86-64 / aarch64), as the reference's LeWriter
+    put(&version, 4);
+    put(&n64, 8);
+    put(&metric, 1);
+    put(&g.k, 4);
+    put(&g.alpha, 4);
+    put(&g.lambda0, 2);
+    for (uint32_t u = 0; u < g.n; ++u) {
+        const uint32_t deg = (uint32_t)(g.offsets[u + 1] - g.offsets[u]);
+        put(&deg, 4);
+        for (uint64_t e = g.offsets[u]; e < g.offsets[u + 1]; ++e) {
+            put(&g.targets[e], 4);
+            put(&g.lambdas[e], 2);
+            put(&g.dists[e], 4);
+        }
+        if (buf.size() > (64u << 20)) {
+            if (std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) {
+                std::fclose(f);
+                fail(TSDG_ERUNTIME, std::string(path) + ": write failed");
+            }
+            buf.clear();
+        }
+    }
+    const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+    if (std::fclose(f) != 0 || !ok) fail(TSDG_ERUNTIME, std::string(path) + ": write failed");
+}
+
 }  // namespace
 
 extern "C" {
@@ -1109,6 +1307,85 @@ int tsdg_gpu_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t
         cuda_check(cudaStreamSynchronize(st), "brute_force_knn");
         cudaStreamDestroy(st);
     });
+}
+
+
+// ---- GPU two-stage diversification --------------------------------------------------
+int tsdg_gpu_build(const float* base, uint32_t n, uint32_t d, const uint32_t* knn_ids,
+                   const float* knn_dists, uint32_t k, float alpha, uint16_t lambda0,
+                   uint32_t max_degree, int metric, int device, tsdg_gpu_graph** out,
+                   uint64_t* stats4) {
+    return guarded([&] {
+        if (!out) fail(TSDG_EINVAL, "build: null out");
+        *out = nullptr;
+        if (!(alpha >= 1.0f)) fail(TSDG_EINVAL, "build: alpha must be >= 1");
+        if (metric < 0 || metric > 2) fail(TSDG_EINVAL, "invalid metric");
+        if (d < 1) fail(TSDG_EINVAL, "build: d must be >= 1");
+        if (k < 1 || k > kDivMaxK) fail(TSDG_EINVAL, "build: GPU path supports 1 <= knn k <= 128");
+        if (n > 0 && (!base || !knn_ids || !knn_dists)) fail(TSDG_EINVAL, "build: null input");
+        auto g = std::make_unique<tsdg_gpu_graph>();
+        g->n = n;
+        g->k = k;
+        g->metric = metric;
+        g->alpha = alpha;
+        g->lambda0 = lambda0;
+        if (n == 0) {
+            g->offsets.assign(1, 0);
+            if (stats4) stats4[0] = stats4[1] = stats4[2] = stats4[3] = 0;
+        } else {
+            DeviceGuard dg(device);
+            cudaStream_t st;
+            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+            try {
+                gpu_build(base, n, d, knn_ids, knn_dists, k, alpha, lambda0, max_degree, metric, *g,
+                          stats4, st);
+            } catch (...) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+                throw;
+            }
+            cudaStreamDestroy(st);
+        }
+        *out = g.release();
+    });
+}
+
+int tsdg_gpu_graph_info(const tsdg_gpu_graph* g, uint64_t* n, uint64_t* num_edges,
+                        uint32_t* max_degree) {
+    return guarded([&] {
+        if (!g) fail(TSDG_EINVAL, "graph_info: null graph");
+        if (n) *n = g->n;
+        if (num_edges) *num_edges = g->targets.size();
+        if (max_degree) {
+            uint32_t m = 0;
+            for (uint32_t u = 0; u < g->n; ++u)
+                m = std::max<uint32_t>(m, (uint32_t)(g->offsets[u + 1] - g->offsets[u]));
+            *max_degree = m;
+        }
+    });
+}
+
+int tsdg_gpu_graph_copy(const tsdg_gpu_graph* g, uint64_t* offsets, uint32_t* targets,
+                        uint16_t* lambdas, float* dists) {
+    return guarded([&] {
+        if (!g) fail(TSDG_EINVAL, "graph_copy: null graph");
+        if (offsets) std::memcpy(offsets, g->offsets.data(), g->offsets.size() * 8);
+        if (targets) std::memcpy(targets, g->targets.data(), g->targets.size() * 4);
+        if (lambdas) std::memcpy(lambdas, g->lambdas.data(), g->lambdas.size() * 2);
+        if (dists) std::memcpy(dists, g->dists.data(), g->dists.size() * 4);
+    });
+}
+
+int tsdg_gpu_graph_save(const tsdg_gpu_graph* g, const char* path) {
+    return guarded([&] {
+        if (!g || !path) fail(TSDG_EINVAL, "graph_save: null argument");
+        write_tsdg_file(*g, path);
+    });
+}
+
+int tsdg_gpu_graph_destroy(tsdg_gpu_graph* g) {
+    delete g;
+    return TSDG_OK;
 }
 
 }  // extern "C"

@@ -13,6 +13,7 @@ Reference interface (paper_2204_00824, /root/reference/proj/include/tsdg):
   ground_truth           bench.hpp (bench.cpp:35-57)  -> ground_truth / GpuIndex.ground_truth
   exact_topk             reference.hpp (reference.cpp:96-111) -> exact_topk
   brute_force_knn        knn_graph.hpp:32             -> brute_force_knn
+  build / save_tsdg      diversify.hpp:114,125        -> build (GPU two-stage diversification)
 Same field names, defaults, argument meaning and exception types
 (std::invalid_argument -> InvalidArgument(ValueError)); results come back as the
 reference's list-of-id-lists, and the extended calls also return fp32 distances
@@ -325,6 +326,49 @@ def brute_force_knn(base, k: int, metric: int = 0, device: int = 0) -> KnnGraph:
     return KnnGraph(n, int(keff.value), ids, dists)
 
 
+@dataclass
+class BuildStats:
+    """tsdg::BuildStats (diversify.hpp:39-44)."""
+    input_edges: int = 0
+    stage1_edges: int = 0
+    augmented_edges: int = 0
+    final_edges: int = 0
+
+
+def build(base, knn: KnnGraph, alpha: float = 1.2, lambda0: int = 9, max_degree: int = 0,
+          metric: int = 0, device: int = 0, save_path: Optional[str] = None,
+          stats: Optional[BuildStats] = None) -> TsdgGraph:
+    """tsdg::build (diversify.cpp:152-209) on the GPU: the same TsdgGraph as the
+    reference's from the same KnnGraph.  save_path writes it in the reference's file
+    format (save_tsdg, diversify.cpp:252-272)."""
+    b = _f32rows(base)
+    ids = np.ascontiguousarray(knn.ids, np.uint32)
+    dists = np.ascontiguousarray(knn.dists, np.float32)
+    if ids.shape[0] != b.shape[0]:
+        raise InvalidArgument("build: graph/set size mismatch")
+    st = (ctypes.c_uint64 * 4)()
+    g = ctypes.c_void_p()
+    check(lib().tsdg_gpu_build(_p(b), b.shape[0], b.shape[1], _p(ids), _p(dists), ids.shape[1],
+                               float(alpha), int(lambda0), int(max_degree), int(metric), device,
+                               ctypes.byref(g), st))
+    try:
+        n, ne, md = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint32()
+        check(lib().tsdg_gpu_graph_info(g, ctypes.byref(n), ctypes.byref(ne), ctypes.byref(md)))
+        off = np.empty(n.value + 1, np.uint64)
+        tgt = np.empty(ne.value, np.uint32)
+        lam = np.empty(ne.value, np.uint16)
+        dst = np.empty(ne.value, np.float32)
+        check(lib().tsdg_gpu_graph_copy(g, _p(off), _p(tgt), _p(lam), _p(dst)))
+        if save_path is not None:
+            check(lib().tsdg_gpu_graph_save(g, str(save_path).encode()))
+    finally:
+        lib().tsdg_gpu_graph_destroy(g)
+    if stats is not None:
+        stats.input_edges, stats.stage1_edges, stats.augmented_edges, stats.final_edges = list(st)
+    return TsdgGraph(int(n.value), int(metric), int(ids.shape[1]), float(np.float32(alpha)),
+                     int(lambda0), off, tgt, lam, dst, int(md.value))
+
+
 def merge_shards_device(ids_ptr: int, dists_ptr: int, counts_ptr: int, shard_base, shards: int,
                         nq: int, k: int, out_ids_ptr: int, out_dists_ptr: int,
                         out_counts_ptr: int, stream: int = 0) -> None:
@@ -381,4 +425,5 @@ __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "Ts
            "GpuIndex", "load_tsdg", "large_batch_search", "bestfirst_search",
            "small_batch_search", "small_batch_search_one", "merge_shards_device",
            "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
+           "BuildStats", "build",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]
