@@ -11,6 +11,9 @@
 // and mirrors the entry points it replaces:
 //   tsdg::large_batch_search  bestfirst_search.hpp:47-51  -> tsdg::gpu::large_batch_search
 //   tsdg::small_batch_search  greedy_search.hpp:55-60     -> tsdg::gpu::small_batch_search
+//   tsdg::ground_truth        bench.cpp:35-57             -> tsdg::gpu::ground_truth
+//   tsdg::brute_force_knn     knn_graph.cpp:64-86         -> tsdg::gpu::brute_force_knn
+//   tsdg::build               diversify.cpp:152-209       -> tsdg::gpu::build
 // with the same argument meaning, the same results (bit-exact in Mode::Deterministic)
 // and the same exception types (std::invalid_argument / std::runtime_error).
 // tsdg::gpu::Index keeps the graph and vectors resident in HBM across calls and adds
@@ -22,8 +25,10 @@
 #include <string>
 #include <vector>
 
+#include "tsdg/bench.hpp"
 #include "tsdg/bestfirst_search.hpp"
 #include "tsdg/diversify.hpp"
+#include "tsdg/knn_graph.hpp"
 #include "tsdg/greedy_search.hpp"
 #include "tsdg/vectors.hpp"
 #include "tsdg_gpu.h"
@@ -173,6 +178,86 @@ inline std::vector<std::vector<NodeId>> small_batch_search(const TsdgGraph& grap
                                                            SearchStats* stats = nullptr) {
     if (queries.d != set.d) throw std::invalid_argument("small_batch_search: dim mismatch");
     return Index(graph, set).small_batch_search(queries, k, params, stats);
+}
+
+/// tsdg::ground_truth (bench.cpp:35-57): exact top-K_gt ids per query, same
+/// (dist, id) order and the same fp32 distances as the reference kernel.
+inline GroundTruth ground_truth(const VectorSet& base, const VectorSet& queries,
+                                std::uint32_t k_gt, Metric metric, int device = 0) {
+    if (queries.d != base.d) throw std::invalid_argument("ground_truth: dim mismatch");
+    require_metric_ready(base, metric);
+    require_metric_ready(queries, metric);
+    std::vector<std::uint32_t> ids(static_cast<std::size_t>(queries.n) * k_gt);
+    check(tsdg_gpu_ground_truth(base.data.data(), base.n, queries.data.data(), queries.n, base.d,
+                                k_gt, static_cast<int>(metric), device, ids.data(), nullptr));
+    GroundTruth gt;
+    gt.k = k_gt;
+    gt.ids.resize(queries.n);
+    for (std::uint32_t q = 0; q < queries.n; ++q)
+        gt.ids[q].assign(ids.begin() + static_cast<std::size_t>(q) * k_gt,
+                         ids.begin() + static_cast<std::size_t>(q + 1) * k_gt);
+    return gt;
+}
+
+/// tsdg::brute_force_knn (knn_graph.cpp:64-86): the same KnnGraph (k clamped to n-1).
+inline KnnGraph brute_force_knn(const VectorSet& set, std::uint32_t k, Metric metric,
+                                int device = 0) {
+    require_metric_ready(set, metric);
+    const std::uint32_t kk = set.n >= 2 ? std::max(1u, std::min(k, set.n - 1)) : 1u;
+    std::vector<std::uint32_t> ids(static_cast<std::size_t>(set.n) * kk);
+    std::vector<float> dists(ids.size());
+    std::uint32_t k_eff = 0;
+    check(tsdg_gpu_brute_force_knn(set.data.data(), set.n, set.d, k, static_cast<int>(metric),
+                                   device, ids.data(), dists.data(), &k_eff));
+    KnnGraph g;
+    g.n = set.n;
+    g.k = k_eff;
+    g.flat.resize(ids.size());
+    for (std::size_t i = 0; i < ids.size(); ++i) g.flat[i] = {ids[i], dists[i]};
+    return g;
+}
+
+/// tsdg::build (diversify.cpp:152-209): the same TsdgGraph from the same KnnGraph.
+inline TsdgGraph build(const VectorSet& set, const KnnGraph& knn, const DiversifyParams& params,
+                       Metric metric, BuildStats* stats = nullptr, int device = 0) {
+    require_metric_ready(set, metric);
+    if (knn.n != set.n) throw std::invalid_argument("build: graph/set size mismatch");
+    std::vector<std::uint32_t> ids(knn.flat.size());
+    std::vector<float> dists(knn.flat.size());
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+        ids[i] = knn.flat[i].id;
+        dists[i] = knn.flat[i].dist;
+    }
+    tsdg_gpu_graph* h = nullptr;
+    std::uint64_t st[4] = {0, 0, 0, 0};
+    check(tsdg_gpu_build(set.data.data(), set.n, set.d, ids.data(), dists.data(), knn.k,
+                         params.alpha, params.lambda0, params.max_degree, static_cast<int>(metric),
+                         device, &h, st));
+    std::uint64_t n = 0, ne = 0;
+    std::uint32_t md = 0;
+    tsdg_gpu_graph_info(h, &n, &ne, &md);
+    TsdgGraph g;
+    g.n = static_cast<std::uint32_t>(n);
+    g.metric = metric;
+    g.k = knn.k;
+    g.alpha = params.alpha;
+    g.lambda0 = params.lambda0;
+    g.offsets.resize(n + 1);
+    std::vector<std::uint32_t> t(ne);
+    std::vector<std::uint16_t> l(ne);
+    std::vector<float> d(ne);
+    const int rc = tsdg_gpu_graph_copy(h, g.offsets.data(), t.data(), l.data(), d.data());
+    tsdg_gpu_graph_destroy(h);
+    check(rc);
+    g.edges.resize(ne);
+    for (std::size_t i = 0; i < ne; ++i) g.edges[i] = {t[i], l[i], d[i]};
+    if (stats) {
+        stats->input_edges = st[0];
+        stats->stage1_edges = st[1];
+        stats->augmented_edges = st[2];
+        stats->final_edges = st[3];
+    }
+    return g;
 }
 
 }  // namespace tsdg::gpu

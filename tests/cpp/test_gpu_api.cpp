@@ -158,6 +158,31 @@ int main() {
         CHECK(gpu::large_batch_search(g2, base, queries, p) == large_batch_search(g, base, queries, p));
         std::remove("/tmp/tsdg_gpu_api.tsdg");
     }
+    {
+        CASE("ground_truth / brute_force_knn / build == reference (bench.cpp, knn_graph.cpp, diversify.cpp)");
+        auto [base, queries] = make_synthetic_split(3000, 120, 20, 6, 0.25f, 77);
+        CHECK(gpu::ground_truth(base, queries, 50, Metric::L2) == ground_truth(base, queries, 50, Metric::L2));
+        const auto knn_ref = brute_force_knn(base, 40, Metric::L2);
+        const auto knn_gpu = gpu::brute_force_knn(base, 40, Metric::L2);
+        CHECK(knn_gpu == knn_ref);
+        for (const DiversifyParams dp : {DiversifyParams{1.2f, 9, 0}, DiversifyParams{1.0f, 4, 12}}) {
+            BuildStats s_ref, s_gpu;
+            const auto g_ref = build(base, knn_ref, dp, Metric::L2, &s_ref);
+            const auto g_gpu = gpu::build(base, knn_gpu, dp, Metric::L2, &s_gpu);
+            CHECK(g_gpu == g_ref);
+            CHECK(s_gpu.stage1_edges == s_ref.stage1_edges && s_gpu.final_edges == s_ref.final_edges &&
+                  s_gpu.augmented_edges == s_ref.augmented_edges);
+        }
+        const auto nnd = nn_descent(base, 24, Metric::L2, 4, 0.7, 3);
+        CHECK(gpu::build(base, nnd, {1.2f, 9, 0}, Metric::L2) == build(base, nnd, {1.2f, 9, 0}, Metric::L2));
+        bool threw = false;
+        try {
+            gpu::build(base, knn_gpu, {0.5f, 9, 0}, Metric::L2);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;
 }
