@@ -441,6 +441,16 @@ class Ref:
                                           ctypes.c_uint32(k), ctypes.c_int(metric), _p(ids), _p(dists)))
         return ids, dists
 
+    def normalized_copy(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty_like(x)
+        self.check(self.so.ref_normalized_copy(_p(x), ctypes.c_uint32(x.shape[0]),
+                                               ctypes.c_uint32(x.shape[1]), _p(out)))
+        return out
+
+    def run_bench_file(self, config_path, csv_out):
+        self.check(self.so.ref_run_bench_file(str(config_path).encode(), str(csv_out).encode()))
+
     def nn_descent(self, base, k, iterations, sample_rate, seed, metric=0):
         b = np.ascontiguousarray(base, np.float32)
         n = b.shape[0]

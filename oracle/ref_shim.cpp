@@ -185,6 +185,19 @@ int ref_build_tsdg(const float* base, std::uint32_t n, std::uint32_t d, int metr
     });
 }
 
+// tsdg::normalized_copy (vectors.cpp:68-80).
+int ref_normalized_copy(const float* data, std::uint32_t n, std::uint32_t d, float* out) {
+    return guarded([&] {
+        const auto v = normalized_copy(make_set(data, n, d));
+        std::copy(v.data.begin(), v.data.end(), out);
+    });
+}
+
+// tsdg::run_bench_file (bench.cpp:189-362), unmodified; writes the CSV.
+int ref_run_bench_file(const char* config_path, const char* csv_out) {
+    return guarded([&] { run_bench_file(config_path, csv_out); });
+}
+
 // tsdg::nn_descent (knn_graph.cpp:141-251) rows: n x k_eff (id, dist).
 int ref_nn_descent(const float* base, std::uint32_t n, std::uint32_t d, int metric,
                    std::uint32_t k, std::uint32_t iterations, double sample_rate,
