@@ -52,6 +52,7 @@ struct BfArgs {
     uint32_t* out_counts;
     tsdg_query_stats* out_stats;
     uint32_t* work_counter;
+    uint32_t work_base;     // counter value at launch (tsdg_gpu.cu next_counter)
     uint32_t dch;           // staged dims per row per round (multiple of 8, <= 128)
     uint32_t slots;         // staged rows per gather round (1..32)
     uint32_t prefetch;      // bit 0: next-chunk rows (L2), bit 1: admitted adjacency (L2)
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, 4) bf_kernel(const BfArgs a) {
 
     for (;;) {
         uint32_t q = 0;
-        if (lane == 0) q = atomicAdd(a.work_counter, 1u);
+        if (lane == 0) q = atomicAdd(a.work_counter, 1u) - a.work_base;
         q = __shfl_sync(kFull, q, 0);
         if (q >= a.nq) break;
 

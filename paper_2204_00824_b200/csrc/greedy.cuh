@@ -39,6 +39,7 @@ struct GrArgs {
     uint32_t* walk_hops;          // nq*t0
     uint32_t* walk_evals;
     uint32_t* work_counter;
+    uint32_t work_base;     // counter value at launch (tsdg_gpu.cu next_counter)
     uint32_t dch, slots;
     uint32_t warp_smem, off_query, off_stage, off_bar;
 };
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
 
     for (;;) {
         uint32_t wk = 0;
-        if (lane == 0) wk = atomicAdd(a.work_counter, 1u);
+        if (lane == 0) wk = atomicAdd(a.work_counter, 1u) - a.work_base;
         wk = __shfl_sync(kFull, wk, 0);
         if (wk >= nwalks) break;
         const uint32_t q = wk / a.t0;

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -107,8 +108,9 @@ struct tsdg_gpu_index {
     uint32_t* adj = nullptr;
     uint16_t* lam = nullptr;
     uint32_t* deg_full = nullptr;
-    uint32_t* counters = nullptr;  // work counters, one per launch slot
-    uint32_t counter_slot = 0;
+    uint32_t* counters = nullptr;  // work counters, one per launch slot (never reset:
+    uint32_t counter_slot = 0;     // each launch starts from the slot's known value)
+    uint32_t counter_val[64] = {};
     std::map<uint32_t, uint32_t*> degcut;
     std::mutex mu;
     cudaStream_t stream = nullptr;   // for the host-pointer entry points
@@ -122,10 +124,51 @@ namespace {
 
 constexpr uint32_t kCounterSlots = 64;
 
-uint32_t* next_counter(tsdg_gpu_index* idx, cudaStream_t st) {
-    uint32_t* c = idx->counters + (idx->counter_slot++ % kCounterSlots);
-    cuda_check(cudaMemsetAsync(c, 0, sizeof(uint32_t), st), "cudaMemsetAsync(counter)");
-    return c;
+// Work-queue tickets without a memset per launch: a persistent kernel hands out work
+// with atomicAdd on its slot and every warp exits after exactly one fetch past the
+// end, so a launch advances the slot by (work items + warps).  The kernel subtracts
+// the slot's value at launch time (`base`).
+struct Ticket {
+    uint32_t* ptr;
+    uint32_t base;
+    uint32_t slot;
+};
+Ticket next_counter(tsdg_gpu_index* idx) {
+    const uint32_t slot = idx->counter_slot++ % kCounterSlots;
+    return Ticket{idx->counters + slot, idx->counter_val[slot], slot};
+}
+void commit_counter(tsdg_gpu_index* idx, const Ticket& t, uint64_t items, uint64_t warps) {
+    idx->counter_val[t.slot] += (uint32_t)(items + warps);
+}
+
+// Cached per-(kernel, device) launch attributes: the host side of a small-batch call
+// is part of its latency.
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_smem_attr;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+void set_smem(const void* kern, size_t smem, const char* what) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& v = g_smem_attr[{kern, cur_device()}];
+    if ((int)smem > v) {
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), what);
+        v = (int)smem;
+    }
+}
+int occupancy(const void* kern, int threads, size_t smem) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    const auto key = std::make_tuple(kern, cur_device(), threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    g_occ[key] = per_sm;
+    return per_sm;
 }
 
 const uint32_t* get_degcut(tsdg_gpu_index* idx, uint32_t cut, cudaStream_t st) {
@@ -208,9 +251,7 @@ BfKernel pick_bf(int metric, bool fast, bool tma, bool kreg) {
 template <class K>
 int grid_for(K kernel, int threads, size_t smem, int sm_count, uint32_t work_warps,
              int warps_per_cta) {
-    int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
-               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), threads, smem);
     if (per_sm < 1) fail(TSDG_ERUNTIME, "kernel does not fit on an SM (shared memory)");
     const uint32_t need = (work_warps + warps_per_cta - 1) / warps_per_cta;
     return (int)std::max<uint32_t>(1, std::min<uint32_t>(need, (uint32_t)(per_sm * sm_count)));
@@ -250,7 +291,9 @@ void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_dists = d_dists;
     a.out_counts = d_counts;
     a.out_stats = d_stats;
-    a.work_counter = next_counter(idx, st);
+    const Ticket tk = next_counter(idx);
+    a.work_counter = tk.ptr;
+    a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
     a.slots = 32;
     // every id the search can touch: <= min(n, 1 + hop_limit * max degree)
@@ -285,9 +328,9 @@ void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     if (idx->metric == 0) kern = fast ? bf_unbounded_kernel<0, true> : bf_unbounded_kernel<0, false>;
     else if (idx->metric == 1) kern = fast ? bf_unbounded_kernel<1, true> : bf_unbounded_kernel<1, false>;
     else kern = fast ? bf_unbounded_kernel<2, true> : bf_unbounded_kernel<2, false>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.warp_smem),
-               "cudaFuncSetAttribute(unbounded)");
+    set_smem(reinterpret_cast<const void*>(kern), a.warp_smem, "cudaFuncSetAttribute(unbounded)");
     kern<<<warps, 32, a.warp_smem, st>>>(a);
+    commit_counter(idx, tk, nq, warps);
     g_launches++;
     cuda_check(cudaGetLastError(), "bf_unbounded_kernel launch");
     int h_over = 0;
@@ -326,7 +369,9 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_dists = d_dists;
     a.out_counts = d_counts;
     a.out_stats = d_stats;
-    a.work_counter = next_counter(idx, st);
+    const Ticket tk = next_counter(idx);
+    a.work_counter = tk.ptr;
+    a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
     a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
     a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
@@ -336,10 +381,10 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     const size_t smem = (size_t)a.warp_smem * wpc;
     const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST,
                                   !env_is("TSDG_STAGE", "ldgsts"), a.k <= 31);
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "cudaFuncSetAttribute(bf)");
+    set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf)");
     const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq, wpc);
     kern<<<grid, wpc * 32, smem, st>>>(a);
+    commit_counter(idx, tk, nq, (uint64_t)grid * wpc);
     g_launches++;
     cuda_check(cudaGetLastError(), "bf_kernel launch");
 }
@@ -398,7 +443,9 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.walk_dists = wb.dists;
     a.walk_hops = wb.hops;
     a.walk_evals = wb.evals;
-    a.work_counter = next_counter(idx, st);
+    const Ticket tk = next_counter(idx);
+    a.work_counter = tk.ptr;
+    a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
     a.slots = 32;
     Carve c;
@@ -418,10 +465,10 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
         kern = fast ? greedy_walk_kernel<1, true, kStageLdgsts> : greedy_walk_kernel<1, false, kStageLdgsts>;
     else
         kern = fast ? greedy_walk_kernel<2, true, kStageLdgsts> : greedy_walk_kernel<2, false, kStageLdgsts>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "cudaFuncSetAttribute(greedy)");
+    set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(greedy)");
     const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq * t0, wpc);
     kern<<<grid, wpc * 32, smem, st>>>(a);
+    commit_counter(idx, tk, (uint64_t)nq * t0, (uint64_t)grid * wpc);
     g_launches++;
     cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
 }
@@ -476,8 +523,7 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
     if (idx->metric == 0) kern = fast ? greedy_cta_kernel<0, true> : greedy_cta_kernel<0, false>;
     else if (idx->metric == 1) kern = fast ? greedy_cta_kernel<1, true> : greedy_cta_kernel<1, false>;
     else kern = fast ? greedy_cta_kernel<2, true> : greedy_cta_kernel<2, false>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "cudaFuncSetAttribute(greedy_cta)");
+    set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(greedy_cta)");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nq * p->t0);
     cfg.blockDim = dim3(kGcThreads);
@@ -485,20 +531,28 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     if (a.cluster) {
-        if (p->t0 > 8)
-            cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                       "cudaFuncSetAttribute(non-portable cluster)");
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = p->t0;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
-            cudaGetLastError();
-            return false;
+        // cluster feasibility per (kernel, device, t0, smem), checked once
+        static std::map<std::tuple<const void*, int, uint32_t, size_t>, bool> ok_cache;
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), cur_device(), p->t0, smem);
+        auto it = ok_cache.find(key);
+        if (it == ok_cache.end()) {
+            if (p->t0 > 8)
+                cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                           "cudaFuncSetAttribute(non-portable cluster)");
+            int nclusters = 0;
+            const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess &&
+                            nclusters >= 1;
+            if (!ok) cudaGetLastError();
+            it = ok_cache.emplace(key, ok).first;
         }
+        if (!it->second) return false;
     }
     cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "greedy_cta_kernel launch");
     g_launches++;
@@ -607,11 +661,8 @@ void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const flo
     const size_t smem = scan_smem(a.P);
     void (*kern)(ScanArgs) = metric == 0 ? exact_scan_kernel<0>
                              : metric == 1 ? exact_scan_kernel<1> : exact_scan_kernel<2>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "cudaFuncSetAttribute(exact_scan)");
-    int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kScanThreads, smem),
-               "occupancy(exact_scan)");
+    set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(exact_scan)");
+    const int per_sm = occupancy(reinterpret_cast<const void*>(kern), kScanThreads, smem);
     const uint32_t slots = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
     const uint32_t qtiles = (nq + kScanQT - 1) / kScanQT;
     // split the base rows so that the grid is >= ~4 waves; each split >= 8 tiles
@@ -1058,11 +1109,13 @@ int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_
         uint32_t* dc = reinterpret_cast<uint32_t*>(base + al(bq) + 2 * al(bi));
         tsdg_query_stats* ds =
             reinterpret_cast<tsdg_query_stats*>(base + al(bq) + 2 * al(bi) + al(bc));
-        // Copy/compute pipeline: the batch is cut into chunks alternating between two
+        // Copy/compute pipeline (2 chunks measured best on C2: 1.27 vs 1.31 ms for 1, 1.32
+        // for 4, TSDG_E2E_CHUNKS overrides): the batch is cut into chunks alternating between two
         // streams, so chunk c+1's upload overlaps chunk c's search and chunk c-1's
         // download.  Each chunk keeps its global query index (RNG stream fork(base+q)).
         get_degcut(idx, params->lambda_cut, idx->stream);
-        const uint32_t nchunks = nq >= 4096 ? 4 : 1;
+        const int env_chunks = env_int("TSDG_E2E_CHUNKS", 0);
+        const uint32_t nchunks = env_chunks > 0 ? (uint32_t)env_chunks : (nq >= 4096 ? 2 : 1);
         const uint32_t csz = (nq + nchunks - 1) / nchunks;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t q0 = c * csz;

@@ -36,6 +36,7 @@ struct UbArgs {
     uint32_t* out_counts;
     tsdg_query_stats* out_stats;
     uint32_t* work_counter;
+    uint32_t work_base;     // counter value at launch (tsdg_gpu.cu next_counter)
     uint32_t dch, slots;
     // per-warp arena in global memory
     uint32_t* hkeys;   // [warps][hcap]
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(32) bf_unbounded_kernel(const UbArgs a) {
 
     for (;;) {
         uint32_t q = 0;
-        if (lane == 0) q = atomicAdd(a.work_counter, 1u);
+        if (lane == 0) q = atomicAdd(a.work_counter, 1u) - a.work_base;
         q = __shfl_sync(kFull, q, 0);
         if (q >= a.nq) break;
         const float* gq = a.queries + (size_t)q * a.d;

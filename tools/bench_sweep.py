@@ -26,6 +26,15 @@ idx = GpuIndex(load_tsdg(ds.graph_path), ds.base)
 print(f"# setup {time.time()-t:.1f}s", flush=True)
 dev = torch.device("cuda:0")
 nq = ds.queries.shape[0]
+# SWEEP_ORDER=pivot<N>: process queries grouped by their nearest of N random base rows
+# (an upper-bound experiment for L2-locality-aware query scheduling)
+if os.environ.get("SWEEP_ORDER", "").startswith("pivot"):
+    npiv = int(os.environ["SWEEP_ORDER"][5:] or 64)
+    piv = ds.base[np.random.default_rng(0).choice(ds.base.shape[0], npiv, replace=False)]
+    d2 = ((ds.queries[:, None, :] - piv[None, :, :]) ** 2).sum(-1)
+    perm = np.argsort(d2.argmin(1), kind="stable")
+    ds.queries[:] = ds.queries[perm]
+    ds.gt[:] = ds.gt[perm]
 dq = torch.from_numpy(ds.queries).to(dev)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 stream = torch.cuda.Stream()
