@@ -157,13 +157,13 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
         float rd = kInf;
         uint32_t ri = kInvalid;
         bool improved = true;
+        uint32_t deg = __ldg(a.degcut + u);
+        uint32_t e_next = (uint32_t)lane < a.R ? __ldg(a.adj + (size_t)u * a.R + lane) : kInvalid;
         while (improved && t < a.hop_limit) {
             ++t;
             float td = kInf;
             uint32_t ti = kInvalid;
             const uint32_t* arow = a.adj + (size_t)u * a.R;
-            const uint32_t deg = __ldg(a.degcut + u);
-            uint32_t e_next = (uint32_t)lane < a.R ? __ldg(arow + lane) : kInvalid;
             for (uint32_t base = 0; base < deg; base += 32) {
                 const uint32_t j = base + lane;
                 const bool valid = j < deg;
@@ -177,11 +177,16 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
                 }
             }
             evals += deg;
-            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
+            // next node = minimum of R_temp (greedy_search.cpp:63-67), known before
+            // merge_halves: its deg_cut entry and first adjacency entries load while
+            // the merge runs
             float nd = td;
             uint32_t ni = ti;
             warp_argmin(nd, ni);
             if (ni != kInvalid) u = ni;
+            deg = __ldg(a.degcut + u);
+            e_next = (uint32_t)lane < a.R ? __ldg(a.adj + (size_t)u * a.R + lane) : kInvalid;
+            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
             improved = updated;
         }
         a.walk_ids[(size_t)wk * 32 + lane] = ri;

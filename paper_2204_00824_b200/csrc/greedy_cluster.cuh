@@ -115,15 +115,19 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     while (ctl->improved && t < a.hop_limit) {
         ++t;
         const uint32_t u = ctl->u;
-        const uint32_t deg = __ldg(a.degcut + u);
         const uint32_t* arow = a.adj + (size_t)u * a.R;
+        // deg and this warp's first adjacency group load together (no deg -> row
+        // dependency on the hop's critical path)
+        const uint32_t j0 = (uint32_t)warp * 32 + lane;
+        const uint32_t e0 = j0 < a.R ? __ldg(arow + j0) : kInvalid;
+        const uint32_t deg = __ldg(a.degcut + u);
         const uint32_t ngroups = (deg + 31) / 32;
         float md = kInf;
         uint32_t mi = kInvalid, mg = 0xFFFFFFFFu;
         for (uint32_t gi = warp; gi < ngroups; gi += kGcWarps) {
             const uint32_t j = gi * 32 + lane;
             const bool valid = j < deg;
-            const uint32_t e = valid ? __ldg(arow + j) : kInvalid;
+            const uint32_t e = valid ? (gi == (uint32_t)warp ? e0 : __ldg(arow + j)) : kInvalid;
             const float dist = gather_eval<METRIC, FAST, kStageTma>(w, g, valid, e, lane);
             if (valid && dist < md) {
                 md = dist;
@@ -145,10 +149,18 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
                     tg = p.group;
                 }
             }
-            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
+            // the next node is the minimum of R_temp (greedy_search.cpp:63-67): known
+            // before merge_halves, so its deg_cut entry and adjacency row are pulled
+            // into L2 while the merge runs (wasted only on the walk's last hop)
             float nd = td;
             uint32_t ni = ti;
             warp_argmin(nd, ni);
+            if (ni != kInvalid) {
+                const char* nrow = reinterpret_cast<const char*>(a.adj + (size_t)ni * a.R);
+                if ((uint32_t)lane * 32u < a.R) prefetch_l2(nrow + lane * 128u);
+                if (lane == 0) prefetch_l2(a.degcut + ni);
+            }
+            const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
             if (lane == 0) {
                 if (ni != kInvalid) ctl->u = ni;
                 ctl->improved = updated ? 1u : 0u;

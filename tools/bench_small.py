@@ -54,6 +54,9 @@ if __name__ == "__main__":
         os.environ["TSDG_GREEDY"] = kern
         for t0 in (8, 16):
             for batch in (1, 8, 64):
-                r = small_batch_latency(idx, ds.queries, ds.gt, batch, GreedyParams(t0=t0, seed=7))
+                mode = int(os.environ.get("MODE", "0"))
+                r = small_batch_latency(idx, ds.queries, ds.gt, batch, GreedyParams(t0=t0, seed=7),
+                                        mode=mode)
                 r["kernel"] = kern
+                r["mode"] = "fast" if mode else "det"
                 print(json.dumps(r), flush=True)
