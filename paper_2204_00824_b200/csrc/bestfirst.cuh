@@ -60,7 +60,7 @@ struct BfArgs {
                             // current bound (0: never; sequential replay only)
     // per-warp shared-memory carve (bytes)
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
-        off_vsize, off_voldest, off_rid, off_rdist, off_bar;
+        off_vsize, off_voldest, off_rid, off_rdist, off_bar, off_rowid;
 };
 
 struct BfWarp {
@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, 4) bf_kernel(const BfArgs a) {
     w.st.stage = reinterpret_cast<float*>(ws + a.off_stage);
     w.st.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
     w.st.parity = 0;
+    w.st.rowid = a.off_rowid ? reinterpret_cast<uint32_t*>(ws + a.off_rowid) : nullptr;
     w.cid = reinterpret_cast<uint32_t*>(ws + a.off_cid);
     w.cdist = reinterpret_cast<float*>(ws + a.off_cdist);
     w.csize = reinterpret_cast<uint32_t*>(ws + a.off_csize);

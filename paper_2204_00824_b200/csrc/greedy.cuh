@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
     w.stage = reinterpret_cast<float*>(ws + a.off_stage);
     w.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
     w.parity = 0;
+    w.rowid = nullptr;
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     if (STAGE == kStageTma) {
         if (lane == 0) mbar_init(w.bar, 1);

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * pitch;
     w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
     w.parity = 0;
+    w.rowid = nullptr;
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     const float kInf = __int_as_float(0x7f800000);
 

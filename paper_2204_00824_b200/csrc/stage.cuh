@@ -32,6 +32,7 @@ struct WarpStage {
     float* stage;   // 32 x (dch + 4)
     uint64_t* bar;  // TMA path
     uint32_t parity;
+    uint32_t* rowid;  // LDGSTS path: row id per slot (32), or nullptr (then __fns)
 };
 
 struct Geom {
@@ -187,14 +188,27 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
                 const uint32_t nvec = cw >> 2;             // 16-byte pieces per row
                 const uint32_t rpi = 32u / nvec;           // rows per warp instruction
                 const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
-                for (uint32_t t = 0; t < nr; t += rpi) {
-                    const uint32_t want = r0 + t + sub;      // rank of the row this lane moves
-                    const bool act = sub < rpi && t + sub < nr;
-                    const int src = act ? __fns(nm, 0, (int)want + 1) : 0;
-                    const uint32_t er = __shfl_sync(kFull, e, src);
-                    if (act)
-                        cp_async16(w.stage + (t + sub) * pitch + piece * 4,
-                                   g.vec + (size_t)er * g.ld + c0 + piece * 4);
+                if (w.rowid) {
+                    // owners publish their row ids by slot; copiers read them back (a
+                    // broadcast LDS) instead of searching the ballot for the owner lane
+                    if (c0 == 0 && mine_round) w.rowid[slot] = e;
+                    __syncwarp();
+                    for (uint32_t t = 0; t < nr; t += rpi) {
+                        const uint32_t row = t + sub;
+                        if (sub < rpi && row < nr)
+                            cp_async16(w.stage + row * pitch + piece * 4,
+                                       g.vec + (size_t)w.rowid[row] * g.ld + c0 + piece * 4);
+                    }
+                } else {
+                    for (uint32_t t = 0; t < nr; t += rpi) {
+                        const uint32_t want = r0 + t + sub;  // rank of the row this lane moves
+                        const bool act = sub < rpi && t + sub < nr;
+                        const int src = act ? __fns(nm, 0, (int)want + 1) : 0;
+                        const uint32_t er = __shfl_sync(kFull, e, src);
+                        if (act)
+                            cp_async16(w.stage + (t + sub) * pitch + piece * 4,
+                                       g.vec + (size_t)er * g.ld + c0 + piece * 4);
+                    }
                 }
                 cp_async_wait_all();
                 __syncwarp();

@@ -216,6 +216,7 @@ void fill_bf_layout(BfArgs& a) {
     const bool kreg = a.k <= 31;
     a.off_rid = c.take(kreg ? 0 : round_up(a.k + 2, 32) * 4);
     a.off_rdist = c.take(kreg ? 0 : round_up(a.k + 2, 32) * 4);
+    a.off_rowid = c.take(32 * 4);
     a.warp_smem = round_up(c.total, 128);
 }
 

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(32) bf_unbounded_kernel(const UbArgs a) {
     w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage);
     w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar);
     w.parity = 0;
+    w.rowid = nullptr;
     if (lane == 0) mbar_init(w.bar, 1);
     __syncwarp();
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
