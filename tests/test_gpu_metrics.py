@@ -1,0 +1,109 @@
+"""Search kernels under the non-L2 metrics (vectors.cpp:10-16: inner product = -dot,
+cosine = 1 - dot on unit rows) and the reference tests' monotonicity properties
+(test_greedy.cpp:264-305 t0 nesting / recall, test_bestfirst.cpp:76-101 Delta), all
+through the C-ABI on the GPU and checked against the oracle (tests only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2204_00824_b200 import _native, datasets
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def index(fixtures):
+    from paper_2204_00824_b200 import search
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            _, b, _ = fixtures(name)
+            cache[name] = search.GpuIndex(search.load_tsdg(os.path.join(GOLDEN, f"{name}.tsdg")), b)
+        return cache[name]
+
+    return get
+
+
+def _same(got, want):
+    np.testing.assert_array_equal(got.ids, want.ids)
+    np.testing.assert_array_equal(got.dists.view(np.uint32), want.dists.view(np.uint32))
+    np.testing.assert_array_equal(got.counts, want.counts)
+
+
+def test_inner_product_graph_search_bit_exact():
+    from paper_2204_00824_b200 import search
+    with open(os.path.join(GOLDEN, "scan.json")) as f:
+        spec = json.load(f)["specs"]["b"]
+    base, queries = datasets.generate(spec)
+    path = os.path.join(GOLDEN, "build_ip_b.tsdg")  # reference build, metric 2
+    g = O.parse_tsdg(path)
+    assert g.metric == 2
+    idx = search.GpuIndex.from_file(path, base)
+    orc = O.Oracle()
+    for p in (search.BestFirstParams(k=10, seed=3), search.BestFirstParams(k=40, seed=4, m_segments=5)):
+        _same(idx.search_bestfirst(queries, p), orc.large_batch(g, base, queries, p))
+    gp = search.GreedyParams(t0=4, seed=9)
+    got = idx.search_greedy(queries, 10, gp)
+    _same(got, orc.small_batch(g, base, queries, 10, gp))
+
+
+def test_cosine_graph_search_bit_exact(tmp_path):
+    from paper_2204_00824_b200 import bench_runner, search
+    base, queries = datasets.make_synthetic_split(1500, 60, 24, 6, 0.3, 13)
+    base, queries = bench_runner.normalized_copy(base), bench_runner.normalized_copy(queries)
+    knn = search.brute_force_knn(base, 20, metric=1)
+    path = str(tmp_path / "cos.tsdg")
+    search.build(base, knn, 1.2, 9, 0, metric=1, save_path=path)
+    g = O.parse_tsdg(path)
+    idx = search.GpuIndex.from_file(path, base)
+    orc = O.Oracle()
+    p = search.BestFirstParams(k=12, seed=5)
+    _same(idx.search_bestfirst(queries, p), orc.large_batch(g, base, queries, p))
+    gp = search.GreedyParams(t0=3, seed=2)
+    _same(idx.search_greedy(queries, 8, gp), orc.small_batch(g, base, queries, 8, gp))
+    # fast mode: recall within the north-star tolerance of the deterministic result
+    gt = search.ground_truth(base, queries, 10, metric=1).ids
+    det = idx.search_bestfirst(queries, p)
+    fast = idx.search_bestfirst(queries, p, mode=_native.MODE_FAST)
+    assert abs(O.recall_at_k(fast.ids, fast.counts, gt, 10) -
+               O.recall_at_k(det.ids, det.counts, gt, 10)) <= 0.005
+
+
+def test_greedy_t0_nesting_and_monotone_recall(fixtures, index):
+    """test_greedy.cpp:264-305: walks s < t0 are the same for every t0 (streams
+    fork(s)), so the t0=4 pool is contained in the t0=8 pool and recall cannot drop."""
+    from paper_2204_00824_b200 import search
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    gt = search.ground_truth(b, q, 10).ids
+    rec = []
+    for t0 in (1, 2, 4, 8, 16):
+        r = idx.search_greedy(q, 10, search.GreedyParams(t0=t0, seed=7))
+        rec.append(O.recall_at_k(r.ids, r.counts, gt, 10))
+    assert all(a <= b + 1e-12 for a, b in zip(rec, rec[1:])), rec
+    # the merged top-k of more walks is never farther, query by query
+    r4 = idx.search_greedy(q, 10, search.GreedyParams(t0=4, seed=7))
+    r8 = idx.search_greedy(q, 10, search.GreedyParams(t0=8, seed=7))
+    assert (r8.dists[:, 0] <= r4.dists[:, 0]).all()
+
+
+def test_bestfirst_delta_monotone(fixtures, index):
+    """test_bestfirst.cpp:76-101: a larger Delta only continues the search longer
+    (with no queue evictions the expansions nest), so hops never decrease and the
+    best distance never gets worse."""
+    from paper_2204_00824_b200 import search
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    prev = None
+    for delta in (0.0, 0.05, 0.5, 1e30):
+        r = idx.search_bestfirst(q, search.BestFirstParams(k=10, seed=3, delta=delta, m_segments=16))
+        if prev is not None:
+            ok = (prev.stats["queue_evictions"] == 0) & (r.stats["queue_evictions"] == 0)
+            assert (r.stats["hops"][ok] >= prev.stats["hops"][ok]).all()
+            assert (r.dists[ok, 0] <= prev.dists[ok, 0]).all()
+        prev = r
