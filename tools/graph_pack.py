@@ -95,7 +95,7 @@ def unpack(pack_path: str, base: np.ndarray, out_path: str) -> None:
     edge_node = np.repeat(np.arange(n, dtype=np.int64), degs)
     edge_pos = node_pos[edge_node] + 4 + 10 * (np.arange(E, dtype=np.int64) - offsets[:-1].astype(np.int64)[edge_node])
     body[edge_pos[:, None] + np.arange(10)[None, :]] = rec
-    tmp = out_path + ".tmp"
+    tmp = f"{out_path}.tmp{os.getpid()}"  # unique per process: ranks may unpack concurrently
     body.tofile(tmp)
     got = _fnv_file(tmp)
     want = str(z["fnv"][0])
