@@ -51,7 +51,7 @@ struct GcArgs {
     int cluster;         // 1: the t0 CTAs of a query form one cluster
     uint32_t npow2;      // pool size for the in-cluster merge
     uint32_t dch, slots;
-    uint32_t off_query, off_stage, off_part, off_bar, off_ctl, off_list, off_pool;
+    uint32_t off_query, off_stage, off_part, off_bar, off_ctl, off_list, off_pool, off_rowid;
 };
 
 struct GcPart {
@@ -66,9 +66,10 @@ struct GcCtl {
     uint32_t improved;
     uint32_t hops;
     uint32_t evals;
+    uint32_t u_next;  // next node, published before the merge (L2 warm-up)
 };
 
-template <int METRIC, bool FAST>
+template <int METRIC, bool FAST, int STAGE>
 __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * pitch;
     w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
     w.parity = 0;
-    w.rowid = nullptr;
+    w.rowid = STAGE == kStageLdgsts ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     const float kInf = __int_as_float(0x7f800000);
 
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     if (warp == 0) {
         const uint64_t st = a.walk_states ? a.walk_states[walk] : fork_state(a.seed, s);
         const uint32_t v = draw_below(st, (uint32_t)lane, a.n);
-        float sd = gather_eval<METRIC, FAST, kStageTma>(w, g, true, v, lane);
+        float sd = gather_eval<METRIC, FAST, STAGE>(w, g, true, v, lane);
         uint32_t si = v;
         warp_argmin(sd, si);
         if (lane == 0) {
@@ -113,6 +114,8 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     float rd = kInf;  // R_ij slot `lane` (warp 0)
     uint32_t ri = kInvalid;
     uint32_t t = 0;
+    PH_DECL
+    PH_MARK(0)  // phase 0: query load + select_start
     while (ctl->improved && t < a.hop_limit) {
         ++t;
         const uint32_t u = ctl->u;
@@ -129,18 +132,23 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
             const uint32_t j = gi * 32 + lane;
             const bool valid = j < deg;
             const uint32_t e = valid ? (gi == (uint32_t)warp ? e0 : __ldg(arow + j)) : kInvalid;
-            const float dist = gather_eval<METRIC, FAST, kStageTma>(w, g, valid, e, lane);
+            const float dist = gather_eval<METRIC, FAST, STAGE>(w, g, valid, e, lane);
             if (valid && dist < md) {
                 md = dist;
                 mi = e;
                 mg = gi;
             }
         }
+        PH_MARK(1)  // adjacency + gather + distances
         part[warp * 32 + lane] = GcPart{md, mi, mg, 0};
         __syncthreads();
+        PH_MARK(2)  // barrier: slowest warp's gather
+        // warp 0 combines the partials into R_temp and finds the next node, the
+        // minimum of R_temp (greedy_search.cpp:63-67) — known before merge_halves
+        float td = kInf;
+        uint32_t ti = kInvalid, ni = kInvalid;
         if (warp == 0) {
-            float td = kInf;
-            uint32_t ti = kInvalid, tg = 0xFFFFFFFFu;
+            uint32_t tg = 0xFFFFFFFFu;
             for (int ww = 0; ww < kGcWarps; ++ww) {
                 const GcPart p = part[ww * 32 + lane];
                 if (p.id == kInvalid) continue;
@@ -150,26 +158,38 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
                     tg = p.group;
                 }
             }
-            // the next node is the minimum of R_temp (greedy_search.cpp:63-67): known
-            // before merge_halves, so its deg_cut entry and adjacency row are pulled
-            // into L2 while the merge runs (wasted only on the walk's last hop)
             float nd = td;
-            uint32_t ni = ti;
+            ni = ti;
             warp_argmin(nd, ni);
-            if (ni != kInvalid) {
-                const char* nrow = reinterpret_cast<const char*>(a.adj + (size_t)ni * a.R);
-                if ((uint32_t)lane * 32u < a.R) prefetch_l2(nrow + lane * 128u);
-                if (lane == 0) prefetch_l2(a.degcut + ni);
-            }
+            if (lane == 0) ctl->u_next = ni;
+        }
+        __syncthreads();
+        if (warp == 0) {
             const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
             if (lane == 0) {
                 if (ni != kInvalid) ctl->u = ni;
                 ctl->improved = updated ? 1u : 0u;
                 ctl->evals += deg;
             }
+        } else {
+            // while warp 0 merges, the other warps pull the next hop's deg_cut entry,
+            // adjacency row and neighbour rows into L2 (wasted only on the last hop)
+            const uint32_t un = ctl->u_next;
+            if (un != kInvalid) {
+                const uint32_t* nrow = a.adj + (size_t)un * a.R;
+                const uint32_t ndeg = __ldg(a.degcut + un);
+                const uint32_t rowb = a.ld * 4u;
+                for (uint32_t j = (uint32_t)(warp - 1) * 32 + lane; j < ndeg; j += (kGcWarps - 1) * 32) {
+                    const char* r = reinterpret_cast<const char*>(a.vec + (size_t)__ldg(nrow + j) * a.ld);
+                    for (uint32_t o = 0; o < rowb; o += 128) prefetch_l2(r + o);
+                }
+            }
         }
+        PH_MARK(3)  // warp 0: combine + merge_halves
         __syncthreads();
+        PH_MARK(4)  // barrier
     }
+    PH_MARK(5)
 
     if (!a.cluster) {
         if (warp == 0) {
@@ -191,6 +211,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     }
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
+    PH_MARK(6)  // waiting for the slowest walk of the query
     if (cluster.block_rank() == 0) {
         float* pd = reinterpret_cast<float*>(smem_raw + a.off_pool);
         uint32_t* pi = reinterpret_cast<uint32_t*>(smem_raw + a.off_pool + a.npow2 * 4);
@@ -283,6 +304,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
             }
         }
     }
+    PH_MARK(7)  // rank 0: pool merge
     cluster.sync();  // siblings stay resident until rank 0 has read their lists
 }
 

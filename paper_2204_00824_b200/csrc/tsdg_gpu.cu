@@ -518,12 +518,22 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
     a.off_part = c.take(kGcThreads * sizeof(GcPart));
     a.off_stage = c.take(kGcWarps * a.slots * (a.dch + 4) * 4, 128);
     a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 : 0);
+    a.off_rowid = c.take(kGcWarps * 32 * 4);
     const size_t smem = round_up(c.total, 128);
     using GcKernel = void (*)(GcArgs);
     GcKernel kern;
-    if (idx->metric == 0) kern = fast ? greedy_cta_kernel<0, true> : greedy_cta_kernel<0, false>;
-    else if (idx->metric == 1) kern = fast ? greedy_cta_kernel<1, true> : greedy_cta_kernel<1, false>;
-    else kern = fast ? greedy_cta_kernel<2, true> : greedy_cta_kernel<2, false>;
+    // row staging: LDGSTS (one coalesced 512 B row per warp instruction) or TMA bulk
+    // copies (issued lane by lane through an ELECT loop); TSDG_GC_STAGE selects
+    const bool ldg = env_is("TSDG_GC_STAGE", "ldgsts");  // measured: TMA 83 us, LDGSTS 92 us
+    if (idx->metric == 0)
+        kern = fast ? (ldg ? greedy_cta_kernel<0, true, kStageLdgsts> : greedy_cta_kernel<0, true, kStageTma>)
+                    : (ldg ? greedy_cta_kernel<0, false, kStageLdgsts> : greedy_cta_kernel<0, false, kStageTma>);
+    else if (idx->metric == 1)
+        kern = fast ? (ldg ? greedy_cta_kernel<1, true, kStageLdgsts> : greedy_cta_kernel<1, true, kStageTma>)
+                    : (ldg ? greedy_cta_kernel<1, false, kStageLdgsts> : greedy_cta_kernel<1, false, kStageTma>);
+    else
+        kern = fast ? (ldg ? greedy_cta_kernel<2, true, kStageLdgsts> : greedy_cta_kernel<2, true, kStageTma>)
+                    : (ldg ? greedy_cta_kernel<2, false, kStageLdgsts> : greedy_cta_kernel<2, false, kStageTma>);
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(greedy_cta)");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nq * p->t0);
