@@ -371,9 +371,25 @@ def main():
     from paper_2204_00824_b200 import datasets
 
     if not datasets.available(DATASET):
-        raise SystemExit(f"data/{DATASET} missing: python tools/make_dataset.py --name {DATASET} "
-                         "--kind lowlid --n 1000000 --nq 10000 --d 128 --latent 16 "
-                         "--builder nndescent --knn-k 64 --iters 5")
+        # data/ is prepared offline (tools/prepare_data.sh); when it is absent (a fresh
+        # checkout) it is rebuilt here, untimed: the graph by the reference's CPU
+        # builder (oracle/_ref, as for every benchmark graph), ground truth on the GPU
+        cmd = [sys.executable, os.path.join(ROOT, "tools", "make_dataset.py"), "--name", DATASET,
+               "--kind", "lowlid", "--n", "1000000", "--nq", "10000", "--d", "128", "--latent", "16",
+               "--builder", "nndescent", "--knn-k", "64", "--iters", "5"]
+        if args.impl != "reference":
+            cmd += ["--gt", "gpu"]
+        if ws > 1:  # one builder; the other ranks wait for its meta.json
+            if rank == 0:
+                subprocess.run(cmd, check=True, stdout=sys.stderr)
+            t_wait = time.time()
+            while not datasets.available(DATASET) and time.time() - t_wait < 3600:
+                time.sleep(5)
+        elif os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtsdg_ref.so")):
+            subprocess.run(cmd, check=True, stdout=sys.stderr)
+        if not datasets.available(DATASET):
+            raise SystemExit(f"data/{DATASET} missing and oracle/_ref is not built: "
+                             "bash tools/prepare_data.sh c2")
     ds = datasets.load(DATASET)
 
     if args.impl == "reference":

@@ -64,6 +64,9 @@ def main() -> None:
     ap.add_argument("--alpha", type=float, default=1.2)
     ap.add_argument("--lambda0", type=int, default=9)
     ap.add_argument("--gt-k", type=int, default=100)
+    ap.add_argument("--gt", choices=["ref", "gpu"], default="ref",
+                    help="ground truth by the reference (CPU) or by the GPU exact scan "
+                         "(bit-identical ids, tests/test_scan.py)")
     args = ap.parse_args()
 
     spec = {
@@ -95,13 +98,17 @@ def main() -> None:
 
     t0 = time.time()
     gt_k = min(args.gt_k, args.n)
-    gt = np.zeros((args.nq, gt_k), np.uint32)
-    rc = ref.ref_ground_truth(
-        base.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint32(args.n),
-        queries.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint32(args.nq),
-        ctypes.c_uint32(args.d), ctypes.c_uint32(gt_k), 0, gt.ctypes.data_as(ctypes.c_void_p))
-    if rc != 0:
-        raise RuntimeError(ref.ref_last_error().decode())
+    if args.gt == "gpu":
+        from paper_2204_00824_b200.search import ground_truth
+        gt = np.ascontiguousarray(ground_truth(base, queries, gt_k).ids)
+    else:
+        gt = np.zeros((args.nq, gt_k), np.uint32)
+        rc = ref.ref_ground_truth(
+            base.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint32(args.n),
+            queries.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint32(args.nq),
+            ctypes.c_uint32(args.d), ctypes.c_uint32(gt_k), 0, gt.ctypes.data_as(ctypes.c_void_p))
+        if rc != 0:
+            raise RuntimeError(ref.ref_last_error().decode())
     gt.tofile(os.path.join(out_dir, "gt.u32"))
     print(f"[make_dataset] ground truth in {time.time()-t0:.1f}s", flush=True)
 
