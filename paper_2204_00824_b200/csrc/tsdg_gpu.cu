@@ -783,9 +783,9 @@ void gpu_build(const float* base, uint32_t n, uint32_t d, const uint32_t* knn_id
                uint32_t max_degree, int metric, tsdg_gpu_graph& g, uint64_t* stats,
                cudaStream_t st) {
     const uint32_t ld = round_up(d, 4);
-    float* vec = upload_rows(base, n, d, ld, st);
     DevBuf<float> vec_keep(0, st);
-    std::swap(vec_keep.p, vec);
+    cudaFreeAsync(vec_keep.p, st);  // adopt the uploaded rows instead
+    vec_keep.p = upload_rows(base, n, d, ld, st);
     DivArgs a{};
     a.vec = vec_keep.p;
     a.n = n;
