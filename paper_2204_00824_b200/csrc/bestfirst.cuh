@@ -111,7 +111,9 @@ __device__ __forceinline__ void v_add(BfWarp& w, uint32_t m, uint32_t u, int lan
     uint32_t* seg = w.vid + s * kSegPitch;
     const uint32_t sz = w.vsize[s];
     const bool hit = lane < (int)sz && seg[lane] == u;
-    if (__ballot_sync(kFull, hit) == 0 && lane == 0) {
+    const unsigned any_hit = __ballot_sync(kFull, hit);
+    __syncwarp();  // every lane's read of the segment before lane 0 writes it
+    if (any_hit == 0 && lane == 0) {
         if (sz < 32) {
             seg[sz] = u;
             w.vsize[s] = sz + 1;
