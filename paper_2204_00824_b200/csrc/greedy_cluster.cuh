@@ -114,21 +114,45 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     float rd = kInf;  // R_ij slot `lane` (warp 0)
     uint32_t ri = kInvalid;
     uint32_t t = 0;
+    // Pipelined hops (TMA staging, whole rows in one round): each warp's first group
+    // of the next hop is issued as soon as the next node is known — while warp 0 runs
+    // merge_halves — and completed at the top of the next hop.
+    const bool pipe = STAGE == kStageTma && a.ld <= a.dch && a.slots >= 32;
+    const uint32_t j0 = (uint32_t)warp * 32 + lane;
+    uint32_t deg = 0, e0 = kInvalid;
+    bool pend = false;  // this lane's row of the pre-issued group
+    if (pipe) {
+        const uint32_t u = ctl->u;
+        deg = __ldg(a.degcut + u);
+        pend = j0 < deg;
+        e0 = pend ? __ldg(a.adj + (size_t)u * a.R + j0) : kInvalid;
+        gather_issue(w, g, pend, e0, lane);
+    }
     PH_DECL
     PH_MARK(0)  // phase 0: query load + select_start
     while (ctl->improved && t < a.hop_limit) {
         ++t;
         const uint32_t u = ctl->u;
         const uint32_t* arow = a.adj + (size_t)u * a.R;
-        // deg and this warp's first adjacency group load together (no deg -> row
-        // dependency on the hop's critical path)
-        const uint32_t j0 = (uint32_t)warp * 32 + lane;
-        const uint32_t e0 = j0 < a.R ? __ldg(arow + j0) : kInvalid;
-        const uint32_t deg = __ldg(a.degcut + u);
+        if (!pipe) {
+            // deg and this warp's first adjacency group load together (no deg -> row
+            // dependency on the hop's critical path)
+            e0 = j0 < a.R ? __ldg(arow + j0) : kInvalid;
+            deg = __ldg(a.degcut + u);
+        }
         const uint32_t ngroups = (deg + 31) / 32;
         float md = kInf;
         uint32_t mi = kInvalid, mg = 0xFFFFFFFFu;
-        for (uint32_t gi = warp; gi < ngroups; gi += kGcWarps) {
+        if (pipe) {  // the first group was issued during the previous hop's merge
+            const float dist = gather_complete<METRIC, FAST>(w, g, pend, lane);
+            if (pend && dist < md) {
+                md = dist;
+                mi = e0;
+                mg = warp;
+            }
+            pend = false;
+        }
+        for (uint32_t gi = pipe ? warp + kGcWarps : warp; gi < ngroups; gi += kGcWarps) {
             const uint32_t j = gi * 32 + lane;
             const bool valid = j < deg;
             const uint32_t e = valid ? (gi == (uint32_t)warp ? e0 : __ldg(arow + j)) : kInvalid;
@@ -164,6 +188,13 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
             if (lane == 0) ctl->u_next = ni;
         }
         __syncthreads();
+        const uint32_t un = ctl->u_next;
+        // next hop (wasted only if the walk stops here): deg + this warp's first group
+        uint32_t ndeg = 0, ne = kInvalid;
+        if (pipe && un != kInvalid) {
+            ndeg = __ldg(a.degcut + un);
+            ne = j0 < a.R ? __ldg(a.adj + (size_t)un * a.R + j0) : kInvalid;
+        }
         if (warp == 0) {
             const bool updated = warp_merge_halves(rd, ri, td, ti, lane);
             if (lane == 0) {
@@ -171,24 +202,28 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
                 ctl->improved = updated ? 1u : 0u;
                 ctl->evals += deg;
             }
-        } else {
+        } else if (!pipe && un != kInvalid) {
             // while warp 0 merges, the other warps pull the next hop's deg_cut entry,
             // adjacency row and neighbour rows into L2 (wasted only on the last hop)
-            const uint32_t un = ctl->u_next;
-            if (un != kInvalid) {
-                const uint32_t* nrow = a.adj + (size_t)un * a.R;
-                const uint32_t ndeg = __ldg(a.degcut + un);
-                const uint32_t rowb = a.ld * 4u;
-                for (uint32_t j = (uint32_t)(warp - 1) * 32 + lane; j < ndeg; j += (kGcWarps - 1) * 32) {
-                    const char* r = reinterpret_cast<const char*>(a.vec + (size_t)__ldg(nrow + j) * a.ld);
-                    for (uint32_t o = 0; o < rowb; o += 128) prefetch_l2(r + o);
-                }
+            const uint32_t* nrow = a.adj + (size_t)un * a.R;
+            const uint32_t nd = __ldg(a.degcut + un);
+            const uint32_t rowb = a.ld * 4u;
+            for (uint32_t j = (uint32_t)(warp - 1) * 32 + lane; j < nd; j += (kGcWarps - 1) * 32) {
+                const char* r = reinterpret_cast<const char*>(a.vec + (size_t)__ldg(nrow + j) * a.ld);
+                for (uint32_t o = 0; o < rowb; o += 128) prefetch_l2(r + o);
             }
+        }
+        if (pipe && un != kInvalid) {
+            deg = ndeg;
+            pend = j0 < ndeg;
+            e0 = pend ? ne : kInvalid;
+            gather_issue(w, g, pend, e0, lane);
         }
         PH_MARK(3)  // warp 0: combine + merge_halves
         __syncthreads();
         PH_MARK(4)  // barrier
     }
+    if (pipe) gather_complete<METRIC, FAST>(w, g, pend, lane);  // drain a pre-issued group
     PH_MARK(5)
 
     if (!a.cluster) {

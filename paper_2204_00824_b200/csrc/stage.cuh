@@ -256,4 +256,54 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
     return result;
 }
 
+// Split form of gather_eval for one round with whole rows (TMA staging, rows of at
+// most dch floats, at most `slots` needed rows): gather_issue starts the copies of the
+// needed rows (rank r -> slot r), gather_complete waits for them and returns each
+// needed lane's distance.  Lets a kernel put a gather in flight ahead of the work
+// that precedes its use (greedy_cta_kernel: the next hop's rows during merge_halves).
+__device__ __forceinline__ void gather_issue(WarpStage& w, const Geom& g, bool need, uint32_t e,
+                                             int lane) {
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return;
+    const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
+    const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(w.bar, __popc(nm) * g.ld * 4u);
+    __syncwarp();
+    if (need) bulk_g2s(w.stage + rank * pitch, g.vec + (size_t)e * g.ld, g.ld * 4u, w.bar);
+}
+
+template <int METRIC, bool FAST>
+__device__ __forceinline__ float gather_complete(WarpStage& w, const Geom& g, bool need, int lane) {
+    const float kInf = __int_as_float(0x7f800000);
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return kInf;
+    const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
+    const uint32_t cnt = __popc(nm);
+    const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
+    mbar_wait(w.bar, w.parity);
+    w.parity ^= 1u;
+    float dist = kInf;
+    if ((uint32_t)lane < cnt) {  // lane r reduces slot r, in the reference's order
+        const float* srow = w.stage + lane * pitch;
+        float acc = 0.0f;
+        unsigned long long acc2 = 0ull;
+        const uint32_t quads = g.d >> 2;
+        row_quads<METRIC, FAST>(srow, w.sq, 0, quads, acc, acc2);
+        for (uint32_t i = quads * 4; i < g.d; ++i) {
+            if (FAST) {
+                const float df = w.sq[i] - srow[i];
+                acc = METRIC == 0 ? fmaf(df, df, acc) : fmaf(w.sq[i], srow[i], acc);
+            } else {
+                acc = acc_exact<METRIC>(acc, w.sq[i], srow[i]);
+            }
+        }
+        dist = FAST ? finish_exact<METRIC>(f2_lo(acc2) + f2_hi(acc2) + acc) : finish_exact<METRIC>(acc);
+    }
+    const float got = __shfl_sync(kFull, dist, (int)(rank & 31u));
+    __syncwarp();
+    return need ? got : kInf;
+}
+
 }  // namespace tsdg_dev

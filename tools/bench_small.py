@@ -52,7 +52,7 @@ if __name__ == "__main__":
     idx = GpuIndex(load_tsdg(ds.graph_path), ds.base)
     for kern in os.environ.get("KERNELS", "cta,warp").split(","):
         os.environ["TSDG_GREEDY"] = kern
-        for t0 in (8, 16):
+        for t0 in [int(x) for x in os.environ.get("T0S", "8,16").split(",")]:
             for batch in (1, 8, 64):
                 mode = int(os.environ.get("MODE", "0"))
                 r = small_batch_latency(idx, ds.queries, ds.gt, batch, GreedyParams(t0=t0, seed=7),
