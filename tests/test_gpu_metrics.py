@@ -107,3 +107,29 @@ def test_bestfirst_delta_monotone(fixtures, index):
             assert (r.stats["hops"][ok] >= prev.stats["hops"][ok]).all()
             assert (r.dists[ok, 0] <= prev.dists[ok, 0]).all()
         prev = r
+
+
+@pytest.mark.parametrize("d", [30, 200])
+def test_odd_and_wide_rows_bit_exact(tmp_path, d):
+    """Rows that are not a multiple of 4 floats (zero-padded to 16 bytes in HBM) and
+    rows wider than one 128-float staging chunk (dimension-chunked gathers, the C4
+    shape) through both procedures, deterministic mode, against the oracle."""
+    from paper_2204_00824_b200 import search
+    base, queries = datasets.make_lowlid(2500, 60, d, 6, 10, 0.25, 31 + d, 0.01)
+    knn = search.brute_force_knn(base, 24)
+    path = str(tmp_path / f"g{d}.tsdg")
+    search.build(base, knn, 1.2, 9, 0, save_path=path)
+    g = O.parse_tsdg(path)
+    idx = search.GpuIndex.from_file(path, base)
+    orc = O.Oracle()
+    for p in (search.BestFirstParams(k=10, seed=1), search.BestFirstParams(k=40, seed=2, m_segments=3)):
+        _same(idx.search_bestfirst(queries, p), orc.large_batch(g, base, queries, p))
+        fast = idx.search_bestfirst(queries, p, mode=_native.MODE_FAST)
+        assert (fast.ids[:, 0] == orc.large_batch(g, base, queries, p).ids[:, 0]).mean() > 0.95
+    for kern in ("cta", "warp"):
+        os.environ["TSDG_GREEDY"] = kern
+        try:
+            gp = search.GreedyParams(t0=4, seed=3)
+            _same(idx.search_greedy(queries, 10, gp), orc.small_batch(g, base, queries, 10, gp))
+        finally:
+            os.environ.pop("TSDG_GREEDY", None)
