@@ -133,3 +133,25 @@ def test_odd_and_wide_rows_bit_exact(tmp_path, d):
             _same(idx.search_greedy(queries, 10, gp), orc.small_batch(g, base, queries, 10, gp))
         finally:
             os.environ.pop("TSDG_GREEDY", None)
+
+
+def test_results_independent_of_launch_shape(fixtures, index, monkeypatch):
+    """acceptance.cpp:376-425 (identical across OpenMP worker counts): the GPU result
+    does not depend on warps per CTA, staging slots, staging path or work order."""
+    from paper_2204_00824_b200 import search
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    p = search.BestFirstParams(k=24, seed=11, m_segments=8)
+    want = idx.search_bestfirst(q, p)
+    for env in ({"TSDG_BF_WARPS": "4"}, {"TSDG_BF_WARPS": "2", "TSDG_SLOTS": "8"},
+                {"TSDG_SLOTS": "32"}, {"TSDG_STAGE": "ldgsts", "TSDG_SLOTS": "24"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        got = idx.search_bestfirst(q, p)
+        _same(got, want)
+        np.testing.assert_array_equal(got.stats, want.stats)
+        for k in env:
+            monkeypatch.delenv(k)
+    # a batch split into uneven pieces with their query_index_base gives the same
+    parts = [idx.search_bestfirst(q[a:c], p, query_index_base=a) for a, c in ((0, 1), (1, 90), (90, 200))]
+    np.testing.assert_array_equal(np.concatenate([r.ids for r in parts]), want.ids)
