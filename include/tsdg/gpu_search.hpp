@@ -160,6 +160,71 @@ private:
     Metric metric_ = Metric::L2;
 };
 
+/// Replicated index over several GPUs of one process: a batch is split into
+/// contiguous slices searched concurrently; identical results for any device list.
+class MultiIndex {
+public:
+    MultiIndex(const TsdgGraph& graph, const VectorSet& base, const std::vector<int>& devices)
+        : d_(base.d) {
+        if (graph.n != base.n)
+            throw std::invalid_argument("gpu::MultiIndex: graph/set size mismatch");
+        std::vector<std::uint32_t> targets(graph.edges.size());
+        std::vector<std::uint16_t> lambdas(graph.edges.size());
+        for (std::size_t i = 0; i < graph.edges.size(); ++i) {
+            targets[i] = graph.edges[i].target;
+            lambdas[i] = graph.edges[i].lambda;
+        }
+        check(tsdg_gpu_multi_create(base.data.data(), base.n, base.d, graph.offsets.data(),
+                                    targets.data(), lambdas.data(), static_cast<int>(graph.metric),
+                                    devices.data(), static_cast<int>(devices.size()), &h_));
+    }
+    MultiIndex(const MultiIndex&) = delete;
+    MultiIndex& operator=(const MultiIndex&) = delete;
+    ~MultiIndex() { tsdg_gpu_multi_destroy(h_); }
+
+    std::vector<std::vector<NodeId>> large_batch_search(const VectorSet& queries,
+                                                        const BestFirstParams& params,
+                                                        SearchStats* stats = nullptr,
+                                                        Mode mode = Mode::Deterministic) const {
+        if (queries.d != d_) throw std::invalid_argument("large_batch_search: dim mismatch");
+        SearchResult r;
+        r.k = params.k;
+        r.ids.resize(static_cast<std::size_t>(queries.n) * params.k);
+        r.dists.resize(r.ids.size());
+        r.counts.resize(queries.n);
+        r.stats.resize(queries.n);
+        const tsdg_bf_params p = to_c(params);
+        check(tsdg_gpu_multi_search_bestfirst(h_, queries.data.data(), queries.n, 0, &p,
+                                              static_cast<int>(mode), r.ids.data(), r.dists.data(),
+                                              r.counts.data(), r.stats.data()));
+        r.add_to(stats);
+        return r.lists();
+    }
+
+    std::vector<std::vector<NodeId>> small_batch_search(const VectorSet& queries, std::uint32_t k,
+                                                        const GreedyParams& params,
+                                                        SearchStats* stats = nullptr,
+                                                        Mode mode = Mode::Deterministic) const {
+        if (queries.d != d_) throw std::invalid_argument("small_batch_search: dim mismatch");
+        SearchResult r;
+        r.k = k;
+        r.ids.resize(static_cast<std::size_t>(queries.n) * k);
+        r.dists.resize(r.ids.size());
+        r.counts.resize(queries.n);
+        r.stats.resize(queries.n);
+        const tsdg_greedy_params p = to_c(params);
+        check(tsdg_gpu_multi_search_greedy(h_, queries.data.data(), queries.n, k, &p,
+                                           static_cast<int>(mode), r.ids.data(), r.dists.data(),
+                                           r.counts.data(), r.stats.data()));
+        r.add_to(stats);
+        return r.lists();
+    }
+
+private:
+    tsdg_gpu_multi* h_ = nullptr;
+    std::uint32_t d_ = 0;
+};
+
 /// Reference-signature free functions (each builds a transient device index).
 inline std::vector<std::vector<NodeId>> large_batch_search(const TsdgGraph& graph,
                                                            const VectorSet& set,

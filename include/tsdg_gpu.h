@@ -159,6 +159,26 @@ int tsdg_gpu_merge_shards_device(const uint32_t* d_ids, const float* d_dists,
                                  uint32_t shards, uint32_t nq, uint32_t k, uint32_t* d_out_ids,
                                  float* d_out_dists, uint32_t* d_out_counts, void* stream);
 
+/* ---- replicated index over several GPUs in one process -----------------------
+ * SURVEY.md §8(b)/(e) "replicate" mode: one device index per entry of `devices`
+ * (built concurrently), each batch split into contiguous slices searched on the
+ * devices concurrently, slice b..e with query_index_base + b, so every query keeps
+ * its reference RNG stream and the results are identical for any device list.
+ * Host pointers, same layouts and errors as the single-device calls.  (The sharded
+ * base layout with an NCCL all-gather lives in the Python layer, shards.py.) */
+typedef struct tsdg_gpu_multi tsdg_gpu_multi;
+int tsdg_gpu_multi_create(const float* base, uint32_t n, uint32_t d, const uint64_t* offsets,
+                          const uint32_t* targets, const uint16_t* lambdas, int metric,
+                          const int* devices, int ndev, tsdg_gpu_multi** out);
+int tsdg_gpu_multi_destroy(tsdg_gpu_multi* m);
+int tsdg_gpu_multi_search_bestfirst(tsdg_gpu_multi* m, const float* queries, uint32_t nq,
+                                    uint64_t query_index_base, const tsdg_bf_params* params,
+                                    int mode, uint32_t* ids, float* dists, uint32_t* counts,
+                                    tsdg_query_stats* stats);
+int tsdg_gpu_multi_search_greedy(tsdg_gpu_multi* m, const float* queries, uint32_t nq, uint32_t k,
+                                 const tsdg_greedy_params* params, int mode, uint32_t* ids,
+                                 float* dists, uint32_t* counts, tsdg_query_stats* stats);
+
 /* ---- exact top-k scan ----------------------------
  * Per query the k smallest (dist, id) pairs over every base row, distances bit-equal
  * to the reference's kernel (sequential fp32, vectors.hpp:36-49), ties by id

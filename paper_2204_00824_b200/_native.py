@@ -72,6 +72,10 @@ SIGNATURES = {
     "tsdg_gpu_graph_copy": (_I, [_VP, _VP, _VP, _VP, _VP]),
     "tsdg_gpu_graph_save": (_I, [_VP, ctypes.c_char_p]),
     "tsdg_gpu_graph_destroy": (_I, [_VP]),
+    "tsdg_gpu_multi_create": (_I, [_VP, _U32, _U32, _VP, _VP, _VP, _I, _VP, _I, _VP]),
+    "tsdg_gpu_multi_destroy": (_I, [_VP]),
+    "tsdg_gpu_multi_search_bestfirst": (_I, [_VP, _VP, _U32, _U64, _VP, _I, _VP, _VP, _VP, _VP]),
+    "tsdg_gpu_multi_search_greedy": (_I, [_VP, _VP, _U32, _U32, _VP, _I, _VP, _VP, _VP, _VP]),
 }
 
 _lib = None

@@ -17,6 +17,7 @@
 #include <memory>
 #include <mutex>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -97,6 +98,11 @@ struct tsdg_gpu_graph {
     std::vector<uint32_t> targets;
     std::vector<uint16_t> lambdas;
     std::vector<float> dists;
+};
+
+// Replicated index over several devices (one tsdg_gpu_index each).
+struct tsdg_gpu_multi {
+    std::vector<tsdg_gpu_index*> parts;
 };
 
 struct tsdg_gpu_index {
@@ -918,6 +924,30 @@ void write_tsdg_file(const tsdg_gpu_graph& g, const char* path) {
 
 }  // namespace
 
+namespace {
+// Runs fn(i) on one host thread per device; returns the first failure (status,
+// message) in device order.
+template <class F>
+void run_per_device(size_t ndev, F&& fn) {
+    std::vector<int> rc(ndev, TSDG_OK);
+    std::vector<std::string> msg(ndev);
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < ndev; ++i)
+        th.emplace_back([&, i] {
+            rc[i] = fn(i);
+            if (rc[i] != TSDG_OK) msg[i] = tsdg_gpu_last_error();
+        });
+    for (auto& t : th) t.join();
+    for (size_t i = 0; i < ndev; ++i)
+        if (rc[i] != TSDG_OK) fail(rc[i], msg[i]);
+}
+// contiguous slice [begin, end) of nq for part i of ndev
+void slice_of(uint32_t nq, size_t ndev, size_t i, uint32_t& b, uint32_t& e) {
+    b = (uint32_t)((uint64_t)nq * i / ndev);
+    e = (uint32_t)((uint64_t)nq * (i + 1) / ndev);
+}
+}  // namespace
+
 extern "C" {
 
 const char* tsdg_gpu_last_error(void) { return g_err.c_str(); }
@@ -1461,6 +1491,86 @@ int tsdg_gpu_graph_save(const tsdg_gpu_graph* g, const char* path) {
 int tsdg_gpu_graph_destroy(tsdg_gpu_graph* g) {
     delete g;
     return TSDG_OK;
+}
+
+
+// ---- replicated multi-device index (one process, several GPUs) ---------------------
+
+int tsdg_gpu_multi_create(const float* base, uint32_t n, uint32_t d, const uint64_t* offsets,
+                          const uint32_t* targets, const uint16_t* lambdas, int metric,
+                          const int* devices, int ndev, tsdg_gpu_multi** out) {
+    return guarded([&] {
+        if (!out) fail(TSDG_EINVAL, "multi_create: null out");
+        *out = nullptr;
+        if (ndev < 1 || !devices) fail(TSDG_EINVAL, "multi_create: need at least one device");
+        auto m = std::make_unique<tsdg_gpu_multi>();
+        m->parts.assign((size_t)ndev, nullptr);
+        try {
+            run_per_device((size_t)ndev, [&](size_t i) {
+                return tsdg_gpu_index_create(base, n, d, offsets, targets, lambdas, metric,
+                                             devices[i], &m->parts[i]);
+            });
+        } catch (...) {
+            for (auto* p : m->parts)
+                if (p) tsdg_gpu_index_destroy(p);
+            throw;
+        }
+        *out = m.release();
+    });
+}
+
+int tsdg_gpu_multi_destroy(tsdg_gpu_multi* m) {
+    if (!m) return TSDG_OK;
+    int rc = TSDG_OK;
+    for (auto* p : m->parts) {
+        const int r = tsdg_gpu_index_destroy(p);
+        if (rc == TSDG_OK) rc = r;
+    }
+    delete m;
+    return rc;
+}
+
+int tsdg_gpu_multi_search_bestfirst(tsdg_gpu_multi* m, const float* queries, uint32_t nq,
+                                    uint64_t query_index_base, const tsdg_bf_params* params,
+                                    int mode, uint32_t* ids, float* dists, uint32_t* counts,
+                                    tsdg_query_stats* stats) {
+    return guarded([&] {
+        if (!m) fail(TSDG_EINVAL, "bestfirst_search: null index");
+        if (nq == 0) return;
+        if (!params) fail(TSDG_EINVAL, "bestfirst_search: null params");
+        if (!queries || !ids) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
+        const uint32_t d = m->parts[0]->d, k = params->k;
+        run_per_device(m->parts.size(), [&](size_t i) {
+            uint32_t b, e;
+            slice_of(nq, m->parts.size(), i, b, e);
+            if (b == e) return (int)TSDG_OK;
+            // query q keeps its stream fork(query_index_base + q): identical results
+            // for any device count
+            return tsdg_gpu_search_bestfirst(m->parts[i], queries + (size_t)b * d, e - b,
+                                             query_index_base + b, params, mode,
+                                             ids + (size_t)b * k, dists ? dists + (size_t)b * k : nullptr,
+                                             counts ? counts + b : nullptr, stats ? stats + b : nullptr);
+        });
+    });
+}
+
+int tsdg_gpu_multi_search_greedy(tsdg_gpu_multi* m, const float* queries, uint32_t nq, uint32_t k,
+                                 const tsdg_greedy_params* params, int mode, uint32_t* ids,
+                                 float* dists, uint32_t* counts, tsdg_query_stats* stats) {
+    return guarded([&] {
+        if (!m) fail(TSDG_EINVAL, "small_batch_search: null index");
+        if (nq == 0) return;
+        if (!queries || !ids) fail(TSDG_EINVAL, "small_batch_search: null buffer");
+        const uint32_t d = m->parts[0]->d;
+        run_per_device(m->parts.size(), [&](size_t i) {
+            uint32_t b, e;
+            slice_of(nq, m->parts.size(), i, b, e);
+            if (b == e) return (int)TSDG_OK;
+            return tsdg_gpu_search_greedy(m->parts[i], queries + (size_t)b * d, e - b, k, params, mode,
+                                          ids + (size_t)b * k, dists ? dists + (size_t)b * k : nullptr,
+                                          counts ? counts + b : nullptr, stats ? stats + b : nullptr);
+        });
+    });
 }
 
 }  // extern "C"

@@ -275,6 +275,65 @@ class GpuIndex:
             ctypes.c_void_p(stream or None)))
 
 
+class MultiGpuIndex:
+    """Replicated index over several GPUs in one process (C-ABI tsdg_gpu_multi): a
+    batch is split into contiguous slices searched concurrently, slice b.. with
+    query_index_base + b — the results equal GpuIndex's for any device list."""
+
+    def __init__(self, graph: TsdgGraph, base, devices=(0,)):
+        base = _f32rows(base)
+        if base.shape[0] != graph.n:
+            raise InvalidArgument(f"graph has {graph.n} nodes, base has {base.shape[0]} rows")
+        self.n, self.d = int(base.shape[0]), int(base.shape[1])
+        devs = np.ascontiguousarray(list(devices), np.int32)
+        h = ctypes.c_void_p()
+        check(lib().tsdg_gpu_multi_create(
+            _p(base), self.n, self.d, _p(np.ascontiguousarray(graph.offsets, np.uint64)),
+            _p(np.ascontiguousarray(graph.targets, np.uint32)),
+            _p(np.ascontiguousarray(graph.lambdas, np.uint16)), int(graph.metric), _p(devs),
+            len(devs), ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            check(lib().tsdg_gpu_multi_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search_bestfirst(self, queries, params: BestFirstParams = BestFirstParams(), *,
+                         query_index_base: int = 0, mode: int = _native.MODE_DETERMINISTIC
+                         ) -> SearchResult:
+        q = _f32rows(queries, self.d)
+        nq, k = q.shape[0], int(params.k)
+        ids = np.empty((nq, max(k, 1)), np.uint32)
+        dists = np.empty((nq, max(k, 1)), np.float32)
+        counts = np.empty(nq, np.uint32)
+        stats = np.zeros(nq, QUERY_STATS_DTYPE)
+        pc = params.c()
+        check(lib().tsdg_gpu_multi_search_bestfirst(self._h, _p(q), nq, query_index_base,
+                                                    ctypes.byref(pc), mode, _p(ids), _p(dists),
+                                                    _p(counts), _p(stats)))
+        return SearchResult(ids, dists, counts, stats)
+
+    def search_greedy(self, queries, k: int, params: GreedyParams = GreedyParams(), *,
+                      mode: int = _native.MODE_DETERMINISTIC) -> SearchResult:
+        q = _f32rows(queries, self.d)
+        nq = q.shape[0]
+        ids = np.empty((nq, max(k, 1)), np.uint32)
+        dists = np.empty((nq, max(k, 1)), np.float32)
+        counts = np.empty(nq, np.uint32)
+        stats = np.zeros(nq, QUERY_STATS_DTYPE)
+        pc = params.c()
+        check(lib().tsdg_gpu_multi_search_greedy(self._h, _p(q), nq, int(k), ctypes.byref(pc), mode,
+                                                 _p(ids), _p(dists), _p(counts), _p(stats)))
+        return SearchResult(ids, dists, counts, stats)
+
+
 @dataclass
 class GroundTruth:
     """tsdg::GroundTruth (bench.hpp): k ids per query, plus the fp32 distances."""
@@ -425,5 +484,5 @@ __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "Ts
            "GpuIndex", "load_tsdg", "large_batch_search", "bestfirst_search",
            "small_batch_search", "small_batch_search_one", "merge_shards_device",
            "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
-           "BuildStats", "build",
+           "BuildStats", "build", "MultiGpuIndex",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]

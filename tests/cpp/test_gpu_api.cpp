@@ -183,6 +183,22 @@ int main() {
         }
         CHECK(threw);
     }
+    {
+        CASE("MultiIndex (replicated over a device list) == reference");
+        auto [base, queries] = make_synthetic_split(2500, 150, 16, 8, 0.2f, 91);
+        const auto g = build(base, brute_force_knn(base, 24, Metric::L2), {1.2f, 9, 0}, Metric::L2);
+        const gpu::MultiIndex multi(g, base, {0, 0, 0});  // three replicas (one GPU here)
+        BestFirstParams p;
+        p.k = 12;
+        p.seed = 4;
+        SearchStats s_ref, s_gpu;
+        CHECK(multi.large_batch_search(queries, p, &s_gpu) == large_batch_search(g, base, queries, p, &s_ref));
+        CHECK(s_gpu.distance_evals == s_ref.distance_evals && s_gpu.hops == s_ref.hops);
+        GreedyParams gp;
+        gp.t0 = 4;
+        gp.seed = 6;
+        CHECK(multi.small_batch_search(queries, 10, gp) == small_batch_search(g, base, queries, 10, gp));
+    }
     std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;
 }

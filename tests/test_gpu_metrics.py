@@ -155,3 +155,23 @@ def test_results_independent_of_launch_shape(fixtures, index, monkeypatch):
     # a batch split into uneven pieces with their query_index_base gives the same
     parts = [idx.search_bestfirst(q[a:c], p, query_index_base=a) for a, c in ((0, 1), (1, 90), (90, 200))]
     np.testing.assert_array_equal(np.concatenate([r.ids for r in parts]), want.ids)
+
+
+def test_multi_device_index_equals_single(fixtures, index):
+    """tsdg_gpu_multi (replicated over a device list; here three replicas on one GPU):
+    each slice keeps its query_index_base, so results equal the single index's."""
+    from paper_2204_00824_b200 import search
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    multi = search.MultiGpuIndex(search.load_tsdg(os.path.join(GOLDEN, "lowlid3k.tsdg")), b,
+                                 devices=(0, 0, 0))
+    p = search.BestFirstParams(k=16, seed=9)
+    for mode in (_native.MODE_DETERMINISTIC, _native.MODE_FAST):
+        want = idx.search_bestfirst(q, p, mode=mode, query_index_base=5)
+        got = multi.search_bestfirst(q, p, mode=mode, query_index_base=5)
+        _same(got, want)
+        np.testing.assert_array_equal(got.stats, want.stats)
+    gp = search.GreedyParams(t0=6, seed=2)
+    _same(multi.search_greedy(q, 10, gp), idx.search_greedy(q, 10, gp))
+    _same(multi.search_bestfirst(q[:2], p), idx.search_bestfirst(q[:2], p))  # fewer queries than devices
+    multi.close()
