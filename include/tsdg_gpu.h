@@ -179,6 +179,23 @@ int tsdg_gpu_multi_search_greedy(tsdg_gpu_multi* m, const float* queries, uint32
                                  const tsdg_greedy_params* params, int mode, uint32_t* ids,
                                  float* dists, uint32_t* counts, tsdg_query_stats* stats);
 
+/* ---- sharded base in one process (the C5 layout) --------------
+ * Shard s: a TSDG over its own rows (local ids, e.g. built by the reference per
+ * shard) and base rows bases[s] (shard_n[s] x d); global id = shard_offset[s] + local.
+ * A search runs every query on every shard (each shard on devices[s], concurrently),
+ * copies the per-shard top-k peer-to-peer to the first shard's device and merges them
+ * there by (dist, global id), first k (merge_shards_kernel).  Host pointers;
+ * ids / dists nq x k, counts nq. */
+typedef struct tsdg_gpu_sharded tsdg_gpu_sharded;
+int tsdg_gpu_sharded_create_from_files(const char* const* tsdg_paths, const float* const* bases,
+                                       const uint32_t* shard_n, const uint64_t* shard_offset,
+                                       uint32_t nshards, uint32_t d, const int* devices,
+                                       tsdg_gpu_sharded** out);
+int tsdg_gpu_sharded_destroy(tsdg_gpu_sharded* sh);
+int tsdg_gpu_sharded_search_bestfirst(tsdg_gpu_sharded* sh, const float* queries, uint32_t nq,
+                                      uint64_t query_index_base, const tsdg_bf_params* params,
+                                      int mode, uint32_t* ids, float* dists, uint32_t* counts);
+
 /* ---- exact top-k scan ----------------------------
  * Per query the k smallest (dist, id) pairs over every base row, distances bit-equal
  * to the reference's kernel (sequential fp32, vectors.hpp:36-49), ties by id

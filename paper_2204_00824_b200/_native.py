@@ -76,6 +76,9 @@ SIGNATURES = {
     "tsdg_gpu_multi_destroy": (_I, [_VP]),
     "tsdg_gpu_multi_search_bestfirst": (_I, [_VP, _VP, _U32, _U64, _VP, _I, _VP, _VP, _VP, _VP]),
     "tsdg_gpu_multi_search_greedy": (_I, [_VP, _VP, _U32, _U32, _VP, _I, _VP, _VP, _VP, _VP]),
+    "tsdg_gpu_sharded_create_from_files": (_I, [_VP, _VP, _VP, _VP, _U32, _U32, _VP, _VP]),
+    "tsdg_gpu_sharded_destroy": (_I, [_VP]),
+    "tsdg_gpu_sharded_search_bestfirst": (_I, [_VP, _VP, _U32, _U64, _VP, _I, _VP, _VP, _VP]),
 }
 
 _lib = None

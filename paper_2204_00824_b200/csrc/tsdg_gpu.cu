@@ -105,6 +105,13 @@ struct tsdg_gpu_multi {
     std::vector<tsdg_gpu_index*> parts;
 };
 
+// Sharded base: one tsdg_gpu_index per shard (local ids), global id = offset + local.
+struct tsdg_gpu_sharded {
+    std::vector<tsdg_gpu_index*> shards;
+    std::vector<uint64_t> offsets;
+    uint32_t d = 0;
+};
+
 struct tsdg_gpu_index {
     int device = 0;
     int sm_count = 148;
@@ -1570,6 +1577,123 @@ int tsdg_gpu_multi_search_greedy(tsdg_gpu_multi* m, const float* queries, uint32
                                           ids + (size_t)b * k, dists ? dists + (size_t)b * k : nullptr,
                                           counts ? counts + b : nullptr, stats ? stats + b : nullptr);
         });
+    });
+}
+
+
+// ---- sharded base in one process (SURVEY.md §8(e), C5 layout) ----------------------
+int tsdg_gpu_sharded_create_from_files(const char* const* tsdg_paths, const float* const* bases,
+                                       const uint32_t* shard_n, const uint64_t* shard_offset,
+                                       uint32_t nshards, uint32_t d, const int* devices,
+                                       tsdg_gpu_sharded** out) {
+    return guarded([&] {
+        if (!out) fail(TSDG_EINVAL, "sharded_create: null out");
+        *out = nullptr;
+        if (nshards < 1 || !tsdg_paths || !bases || !shard_n || !shard_offset || !devices)
+            fail(TSDG_EINVAL, "sharded_create: need at least one shard and its arrays");
+        auto sh = std::make_unique<tsdg_gpu_sharded>();
+        sh->d = d;
+        sh->offsets.assign(shard_offset, shard_offset + nshards);
+        sh->shards.assign(nshards, nullptr);
+        try {
+            run_per_device(nshards, [&](size_t i) {
+                return tsdg_gpu_index_create_from_file(tsdg_paths[i], bases[i], shard_n[i], d,
+                                                       devices[i], &sh->shards[i]);
+            });
+        } catch (...) {
+            for (auto* p : sh->shards)
+                if (p) tsdg_gpu_index_destroy(p);
+            throw;
+        }
+        *out = sh.release();
+    });
+}
+
+int tsdg_gpu_sharded_destroy(tsdg_gpu_sharded* sh) {
+    if (!sh) return TSDG_OK;
+    int rc = TSDG_OK;
+    for (auto* p : sh->shards) {
+        const int r = tsdg_gpu_index_destroy(p);
+        if (rc == TSDG_OK) rc = r;
+    }
+    delete sh;
+    return rc;
+}
+
+int tsdg_gpu_sharded_search_bestfirst(tsdg_gpu_sharded* sh, const float* queries, uint32_t nq,
+                                      uint64_t query_index_base, const tsdg_bf_params* params,
+                                      int mode, uint32_t* ids, float* dists, uint32_t* counts) {
+    return guarded([&] {
+        if (!sh) fail(TSDG_EINVAL, "bestfirst_search: null index");
+        if (nq == 0) return;
+        if (!params) fail(TSDG_EINVAL, "bestfirst_search: null params");
+        if (!queries || !ids) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
+        const uint32_t S = (uint32_t)sh->shards.size(), k = params->k, d = sh->d;
+        // every shard searches every query on its own device; the per-shard top-k
+        // (local ids) are copied peer-to-peer (NVLink) into one [shard][query][k]
+        // block on the first shard's device and merged by (dist, global id) there
+        std::vector<uint32_t*> sid(S, nullptr), scnt(S, nullptr);
+        std::vector<float*> sdist(S, nullptr);
+        std::vector<cudaEvent_t> done(S, nullptr);
+        run_per_device(S, [&](size_t i) {
+            return guarded([&] {
+                tsdg_gpu_index* idx = sh->shards[i];
+                validate_bf(idx, params);
+                std::lock_guard<std::mutex> lk(idx->mu);
+                DeviceGuard dg(idx->device);
+                cudaStream_t st = idx->stream;
+                float* dq = dev_alloc<float>((size_t)nq * d, st);
+                sid[i] = dev_alloc<uint32_t>((size_t)nq * k, st);
+                sdist[i] = dev_alloc<float>((size_t)nq * k, st);
+                scnt[i] = dev_alloc<uint32_t>(nq, st);
+                cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * d * 4, cudaMemcpyHostToDevice, st),
+                           "H2D queries");
+                launch_bestfirst(idx, dq, nq, query_index_base, params, mode, sid[i], sdist[i], scnt[i],
+                                 nullptr, st);
+                cudaFreeAsync(dq, st);
+                cuda_check(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "event");
+                cuda_check(cudaEventRecord(done[i], st), "event record");
+            });
+        });
+        tsdg_gpu_index* m = sh->shards[0];
+        std::lock_guard<std::mutex> lk(m->mu);
+        DeviceGuard dg(m->device);
+        cudaStream_t st = m->stream;
+        const size_t blk = (size_t)nq * k;
+        uint32_t* gid = dev_alloc<uint32_t>(S * blk, st);
+        float* gdist = dev_alloc<float>(S * blk, st);
+        uint32_t* gcnt = dev_alloc<uint32_t>((size_t)S * nq, st);
+        for (uint32_t i = 0; i < S; ++i) {
+            const int dev = sh->shards[i]->device;
+            cuda_check(cudaStreamWaitEvent(st, done[i], 0), "wait shard");
+            cuda_check(cudaMemcpyPeerAsync(gid + i * blk, m->device, sid[i], dev, blk * 4, st), "peer ids");
+            cuda_check(cudaMemcpyPeerAsync(gdist + i * blk, m->device, sdist[i], dev, blk * 4, st), "peer dists");
+            cuda_check(cudaMemcpyPeerAsync(gcnt + (size_t)i * nq, m->device, scnt[i], dev, (size_t)nq * 4, st),
+                       "peer counts");
+        }
+        uint32_t* oid = dev_alloc<uint32_t>(blk, st);
+        float* odist = dev_alloc<float>(blk, st);
+        uint32_t* ocnt = dev_alloc<uint32_t>(nq, st);
+        const int rc = tsdg_gpu_merge_shards_device(gid, gdist, gcnt, sh->offsets.data(), S, nq, k, oid,
+                                                    odist, ocnt, st);
+        if (rc != TSDG_OK) fail(rc, tsdg_gpu_last_error());
+        cuda_check(cudaMemcpyAsync(ids, oid, blk * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+        if (dists) cuda_check(cudaMemcpyAsync(dists, odist, blk * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+        if (counts) cuda_check(cudaMemcpyAsync(counts, ocnt, (size_t)nq * 4, cudaMemcpyDeviceToHost, st), "D2H counts");
+        cuda_check(cudaStreamSynchronize(st), "sharded search");
+        for (uint32_t i = 0; i < S; ++i) {
+            DeviceGuard di(sh->shards[i]->device);
+            cudaFree(sid[i]);
+            cudaFree(sdist[i]);
+            cudaFree(scnt[i]);
+            cudaEventDestroy(done[i]);
+        }
+        cudaFreeAsync(gid, st);
+        cudaFreeAsync(gdist, st);
+        cudaFreeAsync(gcnt, st);
+        cudaFreeAsync(oid, st);
+        cudaFreeAsync(odist, st);
+        cudaFreeAsync(ocnt, st);
     });
 }
 

@@ -334,6 +334,50 @@ class MultiGpuIndex:
         return SearchResult(ids, dists, counts, stats)
 
 
+class ShardedGpuIndex:
+    """Sharded base in one process (C-ABI tsdg_gpu_sharded): shard s = a TSDG file over
+    its own rows, global id = offsets[s] + local id; every query searched on every
+    shard (shard s on devices[s]), per-shard top-k merged by (dist, global id)."""
+
+    def __init__(self, tsdg_paths, bases, offsets, devices=None):
+        self._bases = [_f32rows(b) for b in bases]
+        S = len(self._bases)
+        self.d = int(self._bases[0].shape[1])
+        devs = np.ascontiguousarray(list(devices) if devices is not None else [0] * S, np.int32)
+        paths = (ctypes.c_char_p * S)(*[str(p).encode() for p in tsdg_paths])
+        ptrs = (ctypes.c_void_p * S)(*[b.ctypes.data for b in self._bases])
+        ns = np.ascontiguousarray([b.shape[0] for b in self._bases], np.uint32)
+        offs = np.ascontiguousarray(list(offsets), np.uint64)
+        h = ctypes.c_void_p()
+        check(lib().tsdg_gpu_sharded_create_from_files(paths, ptrs, _p(ns), _p(offs), S, self.d,
+                                                       _p(devs), ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            check(lib().tsdg_gpu_sharded_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search_bestfirst(self, queries, params: BestFirstParams = BestFirstParams(), *,
+                         query_index_base: int = 0, mode: int = _native.MODE_DETERMINISTIC):
+        q = _f32rows(queries, self.d)
+        nq, k = q.shape[0], int(params.k)
+        ids = np.empty((nq, max(k, 1)), np.uint32)
+        dists = np.empty((nq, max(k, 1)), np.float32)
+        counts = np.empty(nq, np.uint32)
+        pc = params.c()
+        check(lib().tsdg_gpu_sharded_search_bestfirst(self._h, _p(q), nq, query_index_base,
+                                                      ctypes.byref(pc), mode, _p(ids), _p(dists),
+                                                      _p(counts)))
+        return ids, dists, counts
+
+
 @dataclass
 class GroundTruth:
     """tsdg::GroundTruth (bench.hpp): k ids per query, plus the fp32 distances."""
@@ -484,5 +528,5 @@ __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "Ts
            "GpuIndex", "load_tsdg", "large_batch_search", "bestfirst_search",
            "small_batch_search", "small_batch_search_one", "merge_shards_device",
            "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
-           "BuildStats", "build", "MultiGpuIndex",
+           "BuildStats", "build", "MultiGpuIndex", "ShardedGpuIndex",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]

@@ -35,3 +35,29 @@ def test_sharded_search_matches_oracle_merge(golden_meta):
         np.testing.assert_array_equal(ids.cpu().numpy().view(np.uint32), wi)
         np.testing.assert_array_equal(dists.cpu().numpy().view(np.uint32), wd.view(np.uint32))
         np.testing.assert_array_equal(counts.cpu().numpy().view(np.uint32), wc)
+
+
+def test_sharded_index_c_abi_matches_oracle_merge(golden_meta):
+    """The in-process sharded index (C-ABI tsdg_gpu_sharded_*, peer copies + device
+    merge; the four shards placed on one GPU here) equals the oracle's per-shard
+    searches merged on the host."""
+    from paper_2204_00824_b200.search import ShardedGpuIndex
+    fx = golden_meta["fixtures"]["shards4"]
+    sb, sq = datasets.generate(dict(fx["spec"], latent=0, noise=0.0))
+    table = [tuple(t) for t in fx["shards"]]
+    paths = [os.path.join(ROOT, "tests", "golden", f"shard4_{s}.tsdg") for s in range(4)]
+    idx = ShardedGpuIndex(paths, [sb[o:o + n] for o, n in table], [o for o, _ in table],
+                          devices=[0, 0, 0, 0])
+    orc = O.Oracle()
+    for p in (BestFirstParams(k=10, seed=21), BestFirstParams(k=32, seed=3, m_segments=4)):
+        ids, dists, counts = idx.search_bestfirst(sq, p, query_index_base=7)
+        res = [orc.large_batch(O.parse_tsdg(paths[s]), sb[o:o + n], sq, p, qbase=7)
+               for s, (o, n) in enumerate(table)]
+        wi, wd, wc = shards.merge_shards_host(np.stack([r.ids for r in res]),
+                                              np.stack([r.dists for r in res]),
+                                              np.stack([r.counts for r in res]),
+                                              [t[0] for t in table], p.k)
+        np.testing.assert_array_equal(ids, wi)
+        np.testing.assert_array_equal(dists.view(np.uint32), wd.view(np.uint32))
+        np.testing.assert_array_equal(counts, wc)
+    idx.close()
