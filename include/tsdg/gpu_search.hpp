@@ -225,6 +225,55 @@ private:
     std::uint32_t d_ = 0;
 };
 
+/// Sharded base in one process: shard s is a TSDG file over its own rows (global id =
+/// offsets[s] + local id) placed on devices[s]; every query is searched on every
+/// shard and the per-shard top-k are merged by (dist, global id) on the device.
+class ShardedIndex {
+public:
+    ShardedIndex(const std::vector<std::string>& tsdg_paths, const std::vector<VectorSet>& bases,
+                 const std::vector<std::uint64_t>& offsets, const std::vector<int>& devices)
+        : d_(bases.empty() ? 0 : bases[0].d) {
+        if (tsdg_paths.size() != bases.size() || offsets.size() != bases.size() ||
+            devices.size() != bases.size() || bases.empty())
+            throw std::invalid_argument("gpu::ShardedIndex: one path, base, offset and device per shard");
+        std::vector<const char*> paths;
+        std::vector<const float*> ptrs;
+        std::vector<std::uint32_t> ns;
+        for (std::size_t s = 0; s < bases.size(); ++s) {
+            paths.push_back(tsdg_paths[s].c_str());
+            ptrs.push_back(bases[s].data.data());
+            ns.push_back(bases[s].n);
+        }
+        check(tsdg_gpu_sharded_create_from_files(paths.data(), ptrs.data(), ns.data(), offsets.data(),
+                                                 static_cast<std::uint32_t>(bases.size()), d_,
+                                                 devices.data(), &h_));
+    }
+    ShardedIndex(const ShardedIndex&) = delete;
+    ShardedIndex& operator=(const ShardedIndex&) = delete;
+    ~ShardedIndex() { tsdg_gpu_sharded_destroy(h_); }
+
+    /// ids (global) per query, ascending by (dist, id), at most params.k.
+    std::vector<std::vector<NodeId>> large_batch_search(const VectorSet& queries,
+                                                        const BestFirstParams& params,
+                                                        Mode mode = Mode::Deterministic) const {
+        if (queries.d != d_) throw std::invalid_argument("large_batch_search: dim mismatch");
+        SearchResult r;
+        r.k = params.k;
+        r.ids.resize(static_cast<std::size_t>(queries.n) * params.k);
+        r.dists.resize(r.ids.size());
+        r.counts.resize(queries.n);
+        const tsdg_bf_params p = to_c(params);
+        check(tsdg_gpu_sharded_search_bestfirst(h_, queries.data.data(), queries.n, 0, &p,
+                                                static_cast<int>(mode), r.ids.data(), r.dists.data(),
+                                                r.counts.data()));
+        return r.lists();
+    }
+
+private:
+    tsdg_gpu_sharded* h_ = nullptr;
+    std::uint32_t d_ = 0;
+};
+
 /// Reference-signature free functions (each builds a transient device index).
 inline std::vector<std::vector<NodeId>> large_batch_search(const TsdgGraph& graph,
                                                            const VectorSet& set,
