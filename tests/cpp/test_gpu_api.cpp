@@ -199,6 +199,47 @@ int main() {
         gp.seed = 6;
         CHECK(multi.small_batch_search(queries, 10, gp) == small_batch_search(g, base, queries, 10, gp));
     }
+    {
+        CASE("ShardedIndex == per-shard reference searches merged by (dist, global id)");
+        auto [base, queries] = make_synthetic_split(3000, 80, 12, 6, 0.25f, 57);
+        const std::uint32_t half = 1400;
+        std::vector<VectorSet> parts(2);
+        std::vector<std::uint64_t> offs = {0, half};
+        std::vector<std::string> paths = {"/tmp/tsdg_shard0.tsdg", "/tmp/tsdg_shard1.tsdg"};
+        std::vector<TsdgGraph> gs;
+        for (int s = 0; s < 2; ++s) {
+            const std::uint32_t lo = s ? half : 0, hi = s ? base.n : half;
+            parts[s].n = hi - lo;
+            parts[s].d = base.d;
+            parts[s].data.assign(base.data.begin() + (std::size_t)lo * base.d, base.data.begin() + (std::size_t)hi * base.d);
+            gs.push_back(build(parts[s], brute_force_knn(parts[s], 20, Metric::L2), {1.2f, 9, 0}, Metric::L2));
+            save_tsdg(gs.back(), paths[s]);
+        }
+        const gpu::ShardedIndex sharded(paths, parts, offs, {0, 0});
+        BestFirstParams p;
+        p.k = 8;
+        p.seed = 13;
+        const auto got = sharded.large_batch_search(queries, p);
+        const auto kernel = kernel_for(Metric::L2);
+        bool same = got.size() == queries.n;
+        for (std::uint32_t q = 0; q < queries.n && same; ++q) {
+            std::vector<IdDist> pool;
+            for (int s = 0; s < 2; ++s) {
+                // query q keeps its stream fork(q) on every shard
+                const auto ids = bestfirst_search(gs[s], parts[s], std::span<const float>(queries.row(q), queries.d),
+                                                  p, Rng64(p.seed).fork(q));
+                for (NodeId id : ids)
+                    pool.push_back({static_cast<NodeId>(id + offs[s]), kernel(queries.row(q), parts[s].row(id), base.d)});
+            }
+            std::sort(pool.begin(), pool.end(), [](const IdDist& a, const IdDist& b) { return closer(a, b); });
+            std::vector<NodeId> want;
+            for (std::size_t i = 0; i < pool.size() && i < p.k; ++i) want.push_back(pool[i].id);
+            same = got[q] == want;
+        }
+        CHECK(same);
+        std::remove(paths[0].c_str());
+        std::remove(paths[1].c_str());
+    }
     std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;
 }
