@@ -94,6 +94,16 @@ public:
                                     static_cast<int>(graph.metric), device, &h_));
         metric_ = graph.metric;
     }
+    /// From a reference .tsdg file and an fvecs/bvecs base, decoded on the device
+    /// (load_tsdg + load_vectors without the host copies; tsdg_gpu_index_create_from_files).
+    Index(const std::string& tsdg_path, const std::string& vectors_path, int device = 0) {
+        check(tsdg_gpu_index_create_from_files(tsdg_path.c_str(), vectors_path.c_str(), device, &h_));
+        std::uint32_t n = 0, d = 0, maxdeg = 0, rs = 0, as = 0;
+        int metric = 0, dev = 0;
+        check(tsdg_gpu_index_info(h_, &n, &d, &metric, &maxdeg, &dev, &rs, &as));
+        d_ = d;
+        metric_ = static_cast<Metric>(metric);
+    }
     Index(const Index&) = delete;
     Index& operator=(const Index&) = delete;
     ~Index() { tsdg_gpu_index_destroy(h_); }

@@ -97,6 +97,16 @@ int tsdg_read_tsdg_header(const char* path, tsdg_graph_header* out);
 int tsdg_read_tsdg(const char* path, uint64_t* offsets, uint32_t* targets,
                    uint16_t* lambdas, float* dists);
 
+/* ---- vector files (replaces load_vectors / load_fvecs / load_bvecs, io.hpp:11-19,
+ * io.cpp:58-121) ------------------------------------------------------------
+ * fvecs (int32 d, d x f32) or, for a ".bvecs" path, bvecs (int32 d, d x u8,
+ * widened to f32).  tsdg_read_vectors_shape reads (n, d) from the first record and
+ * the file size; tsdg_read_vectors fills a caller n x d buffer.  Errors carry the
+ * reference's messages (truncation, implausible / invalid / inconsistent
+ * dimension, non-finite value, empty dataset) as TSDG_ERUNTIME. */
+int tsdg_read_vectors_shape(const char* path, uint32_t* n, uint32_t* d);
+int tsdg_read_vectors(const char* path, float* out, uint32_t n, uint32_t d);
+
 /* ---- device index -----------------------------------------------------------
  * Uploads the fp32 vector store (rows padded to 16 B) and a fixed-degree padded
  * adjacency (row stride = max degree rounded up to 4, CSR order kept exactly,
@@ -107,6 +117,14 @@ int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint6
                           int device, tsdg_gpu_index** out);
 int tsdg_gpu_index_create_from_file(const char* tsdg_path, const float* base, uint32_t n,
                                     uint32_t d, int device, tsdg_gpu_index** out);
+/* Direct file -> HBM index: the raw bytes of a reference .tsdg
+ * file (load_tsdg, diversify.cpp:274-306) and an fvecs/bvecs base (load_vectors,
+ * io.cpp:112-117) are streamed through pinned staging buffers and decoded on the
+ * device into the search layout; no host-side CSR or VectorSet is built.  The
+ * metric comes from the TSDG header.  Same index as tsdg_gpu_index_create on the
+ * decoded arrays. */
+int tsdg_gpu_index_create_from_files(const char* tsdg_path, const char* vectors_path, int device,
+                                     tsdg_gpu_index** out);
 int tsdg_gpu_index_destroy(tsdg_gpu_index* idx);
 /* n, d, metric, max_degree, device, padded row stride (floats), adjacency stride */
 int tsdg_gpu_index_info(const tsdg_gpu_index* idx, uint32_t* n, uint32_t* d, int* metric,

@@ -448,6 +448,16 @@ class Ref:
                                                ctypes.c_uint32(x.shape[1]), _p(out)))
         return out
 
+    def load_vectors(self, path):
+        """tsdg::load_vectors -> (n, d) float32; raises with the reference's message."""
+        n, d = ctypes.c_uint32(), ctypes.c_uint32()
+        self.check(self.so.ref_load_vectors(str(path).encode(), ctypes.byref(n), ctypes.byref(d),
+                                            None))
+        out = np.empty((n.value, d.value), np.float32)
+        self.check(self.so.ref_load_vectors(str(path).encode(), ctypes.byref(n), ctypes.byref(d),
+                                            _p(out)))
+        return out
+
     def run_bench_file(self, config_path, csv_out):
         self.check(self.so.ref_run_bench_file(str(config_path).encode(), str(csv_out).encode()))
 

@@ -29,6 +29,7 @@
 #include "tsdg/bestfirst_search.hpp"
 #include "tsdg/diversify.hpp"
 #include "tsdg/greedy_search.hpp"
+#include "tsdg/io.hpp"
 #include "tsdg/knn_graph.hpp"
 #include "tsdg/rank_list.hpp"
 #include "tsdg/reference.hpp"
@@ -190,6 +191,16 @@ int ref_normalized_copy(const float* data, std::uint32_t n, std::uint32_t d, flo
     return guarded([&] {
         const auto v = normalized_copy(make_set(data, n, d));
         std::copy(v.data.begin(), v.data.end(), out);
+    });
+}
+
+// tsdg::load_vectors (io.cpp:112-117): shape first (out == NULL), then the data.
+int ref_load_vectors(const char* path, std::uint32_t* n, std::uint32_t* d, float* out) {
+    return guarded([&] {
+        const VectorSet v = load_vectors(path);
+        *n = v.n;
+        *d = v.d;
+        if (out) std::copy(v.data.begin(), v.data.end(), out);
     });
 }
 

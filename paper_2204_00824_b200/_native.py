@@ -49,6 +49,9 @@ SIGNATURES = {
     "tsdg_read_tsdg": (_I, [ctypes.c_char_p, _VP, _VP, _VP, _VP]),
     "tsdg_gpu_index_create": (_I, [_VP, _U32, _U32, _VP, _VP, _VP, _I, _I, _VP]),
     "tsdg_gpu_index_create_from_file": (_I, [ctypes.c_char_p, _VP, _U32, _U32, _I, _VP]),
+    "tsdg_gpu_index_create_from_files": (_I, [ctypes.c_char_p, ctypes.c_char_p, _I, _VP]),
+    "tsdg_read_vectors_shape": (_I, [ctypes.c_char_p, _VP, _VP]),
+    "tsdg_read_vectors": (_I, [ctypes.c_char_p, _VP, _U32, _U32]),
     "tsdg_gpu_index_destroy": (_I, [_VP]),
     "tsdg_gpu_index_info": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "tsdg_gpu_deg_cut": (_I, [_VP, _U32, _VP]),

@@ -5,15 +5,20 @@
 // (bestfirst_search.cpp:112-150, greedy_search.cpp:74-127), sizes the
 // persistent kernels for occupancy on the B200's 148 SMs and launches them.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
+#include <utility>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -27,6 +32,7 @@
 #include "diversify.cuh"
 #include "exact_scan.cuh"
 #include "greedy_cluster.cuh"
+#include "loader.cuh"
 #include "unbounded.cuh"
 
 using namespace tsdg_dev;
@@ -955,6 +961,252 @@ void slice_of(uint32_t nq, size_t ndev, size_t i, uint32_t& b, uint32_t& e) {
 }
 }  // namespace
 
+// tsdg_io.cpp (host parsing; error messages in the reference's wording)
+uint32_t tsdg_vector_component_bytes(const std::string& path);
+int tsdg_vector_file_shape(const std::string& path, uint32_t* n, uint32_t* d, std::string& err);
+int tsdg_parse_vector_file(const std::string& path, float* out, uint32_t* n, uint32_t* d,
+                           std::string& err);
+int tsdg_parse_header_bytes(const std::string& path, const unsigned char* p, size_t size,
+                            tsdg_graph_header* h, uint64_t* body_off, std::string& err);
+std::string tsdg_truncated_message(const std::string& path, uint64_t file_size);
+
+namespace {
+
+// Frees whatever an index holds (also a partially built one).
+void free_index(tsdg_gpu_index* idx) {
+    DeviceGuard dg(idx->device);
+    if (idx->stream) cudaStreamSynchronize(idx->stream);
+    if (idx->stream2) cudaStreamSynchronize(idx->stream2);
+    for (auto& kv : idx->degcut) cudaFree(kv.second);
+    if (idx->scratch) cudaFree(idx->scratch);
+    cudaFree(idx->vec);
+    cudaFree(idx->adj);
+    cudaFree(idx->lam);
+    cudaFree(idx->deg_full);
+    cudaFree(idx->counters);
+    if (idx->stream) cudaStreamDestroy(idx->stream);
+    if (idx->stream2) cudaStreamDestroy(idx->stream2);
+    delete idx;
+}
+struct IndexOwner {
+    tsdg_gpu_index* p = new tsdg_gpu_index();
+    ~IndexOwner() {
+        if (p) free_index(p);
+    }
+    tsdg_gpu_index* release() { return std::exchange(p, nullptr); }
+};
+
+// Device, streams, the stream-ordered pool policy and the work counters.
+void init_index_runtime(tsdg_gpu_index* idx, int device) {
+    idx->device = device;
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    idx->sm_count = prop.multiProcessorCount;
+    cuda_check(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&idx->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+    // keep stream-ordered allocations cached across calls (no re-mapping per search)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cuda_check(cudaMalloc(&idx->counters, kCounterSlots * 4), "cudaMalloc(counters)");
+    cuda_check(cudaMemset(idx->counters, 0, kCounterSlots * 4), "cudaMemset(counters)");
+}
+
+// File byte ranges -> device, through two pinned staging buffers: the read of
+// chunk i+1 (split over several threads) overlaps the H2D copy and the decode of
+// chunk i.  push() copies into the stager's own device buffer and enqueues
+// decode(dev) after it (stream order protects the buffer); push_to() copies
+// straight to a caller device address.  visit(host, bytes) runs on the host copy
+// while its H2D copy is in flight.
+// Two pinned host buffers + their copy-done events, shared by the loads of one call.
+struct PinnedPair {
+    size_t bytes;
+    cudaStream_t st;
+    unsigned char* host[2] = {};
+    cudaEvent_t done[2] = {};
+    uint64_t next = 0;  // alternates across the stagers that share the pair
+    PinnedPair(size_t b, cudaStream_t s) : bytes(b), st(s) {
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaMallocHost(&host[i], bytes), "cudaMallocHost(stager)");
+            cuda_check(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
+        }
+    }
+    ~PinnedPair() {
+        cudaStreamSynchronize(st);
+        for (int i = 0; i < 2; ++i) {
+            if (host[i]) cudaFreeHost(host[i]);
+            if (done[i]) cudaEventDestroy(done[i]);
+        }
+    }
+};
+
+class FileStager {
+public:
+    FileStager(const std::string& path, PinnedPair& pin, bool dev_buffers)
+        : path_(path), chunk_(pin.bytes), st_(pin.st), pin_(pin) {
+        fd_ = open(path.c_str(), O_RDONLY);
+        if (fd_ < 0) fail(TSDG_ERUNTIME, path + ": cannot open for reading");
+        struct stat sb {};
+        if (fstat(fd_, &sb) != 0) fail(TSDG_ERUNTIME, path + ": cannot stat");
+        size_ = (uint64_t)sb.st_size;
+        for (int b = 0; b < 2; ++b) {
+            host_[b] = pin.host[b];
+            done_[b] = pin.done[b];
+            if (dev_buffers) cuda_check(cudaMalloc(&dev_[b], chunk_), "cudaMalloc(stager)");
+        }
+    }
+    ~FileStager() {
+        cudaStreamSynchronize(st_);
+        for (int b = 0; b < 2; ++b)
+            if (dev_[b]) cudaFree(dev_[b]);
+        if (fd_ >= 0) close(fd_);
+    }
+    uint64_t size() const { return size_; }
+    void read_at(uint64_t off, size_t bytes, unsigned char* dst) {
+        // a few threads per chunk: one pread stream does not saturate the page cache
+        constexpr size_t kPart = 8ull << 20;
+        const size_t parts = std::min<size_t>(8, (bytes + kPart - 1) / kPart);
+        std::vector<std::thread> th;
+        std::atomic<bool> ok{true};
+        auto part = [&](size_t i) {
+            const size_t b0 = bytes * i / parts, b1 = bytes * (i + 1) / parts;
+            size_t got = b0;
+            while (got < b1) {
+                const ssize_t r = pread(fd_, dst + got, b1 - got, (off_t)(off + got));
+                if (r <= 0) {
+                    ok = false;
+                    return;
+                }
+                got += (size_t)r;
+            }
+        };
+        for (size_t i = 1; i < parts; ++i) th.emplace_back(part, i);
+        if (parts) part(0);
+        for (auto& t : th) t.join();
+        if (!ok) fail(TSDG_ERUNTIME, path_ + ": read failed near byte offset " + std::to_string(off));
+    }
+    template <class Decode, class Visit>
+    void push(uint64_t off, size_t bytes, Decode&& decode, Visit&& visit) {
+        const int b = stage(off, bytes);
+        cuda_check(cudaMemcpyAsync(dev_[b], host_[b], bytes, cudaMemcpyHostToDevice, st_), "H2D file chunk");
+        cuda_check(cudaEventRecord(done_[b], st_), "cudaEventRecord");
+        decode(static_cast<const unsigned char*>(dev_[b]));
+        visit(static_cast<const unsigned char*>(host_[b]), bytes);
+    }
+    template <class Visit>
+    void push_to(uint64_t off, size_t bytes, unsigned char* dst, Visit&& visit) {
+        const int b = stage(off, bytes);
+        cuda_check(cudaMemcpyAsync(dst, host_[b], bytes, cudaMemcpyHostToDevice, st_), "H2D file chunk");
+        cuda_check(cudaEventRecord(done_[b], st_), "cudaEventRecord");
+        visit(static_cast<const unsigned char*>(host_[b]), bytes);
+    }
+
+private:
+    int stage(uint64_t off, size_t bytes) {
+        const int b = (int)(pin_.next++ & 1);
+        cuda_check(cudaEventSynchronize(done_[b]), "stager wait");  // H2D from host_[b] finished
+        read_at(off, bytes, host_[b]);
+        return b;
+    }
+    std::string path_;
+    size_t chunk_;
+    cudaStream_t st_;
+    PinnedPair& pin_;
+    int fd_ = -1;
+    uint64_t size_ = 0;
+    unsigned char* host_[2] = {};
+    unsigned char* dev_[2] = {};
+    cudaEvent_t done_[2] = {};
+};
+
+constexpr size_t kStageChunk = 32ull << 20;
+
+int decode_grid(const tsdg_gpu_index* idx) { return idx->sm_count * 8; }
+
+// vectors file -> idx->vec (n x ld, zero padded); d_bad <- first bad record
+void load_vectors_to_device(tsdg_gpu_index* idx, const std::string& path, PinnedPair& pin,
+                            unsigned long long* d_bad) {
+    const uint32_t cb = tsdg_vector_component_bytes(path);
+    const uint64_t rec = 4ull + (uint64_t)cb * idx->d;
+    const uint32_t per = (uint32_t)std::max<uint64_t>(1, pin.bytes / rec);
+    if (per * rec > pin.bytes) fail(TSDG_ERUNTIME, path + ": record exceeds the staging chunk");
+    FileStager fs(path, pin, true);
+    for (uint32_t r0 = 0; r0 < idx->n; r0 += per) {
+        const uint32_t nr = std::min(per, idx->n - r0);
+        fs.push((uint64_t)r0 * rec, (size_t)nr * rec,
+                [&](const unsigned char* dev) {
+                    unpack_vectors_kernel<<<decode_grid(idx), 256, 0, idx->stream>>>(
+                        dev, nr, r0, idx->d, cb, idx->ld, idx->vec, d_bad);
+                    g_launches++;
+                    cuda_check(cudaGetLastError(), "unpack_vectors_kernel launch");
+                },
+                [](const unsigned char*, size_t) {});
+    }
+}
+
+// TSDG file -> idx->adj / lam / deg_full in ONE read of the file: the body streams
+// into a transient device copy while the host walks the degree fields of each
+// staged chunk (node byte offsets, max degree, truncation check); then the node
+// offsets go up and one decode kernel builds the padded rows.
+void load_graph_to_device(tsdg_gpu_index* idx, const std::string& path, uint64_t body_off,
+                          PinnedPair& pin, unsigned long long* d_bad) {
+    FileStager fs(path, pin, false);
+    const uint64_t body = fs.size() > body_off ? fs.size() - body_off : 0;
+    DevBuf<unsigned char> raw(std::max<uint64_t>(body, 1), idx->stream);
+    std::vector<uint64_t> node_off((size_t)idx->n + 1);
+    uint64_t pos = 0;  // body offset of the next node record
+    uint32_t u = 0, maxdeg = 0;
+    unsigned char tail[4] = {};  // the 4 body bytes before the current chunk
+    uint64_t cs = 0;             // current chunk start (body offset)
+    auto walk = [&](const unsigned char* h, size_t bytes) {
+        const uint64_t ce = cs + bytes;
+        auto byte_at = [&](uint64_t x) { return x >= cs ? h[x - cs] : tail[4 - (cs - x)]; };
+        while (u < idx->n && pos + 4 <= ce) {
+            const uint32_t deg = uint32_t(byte_at(pos)) | uint32_t(byte_at(pos + 1)) << 8 |
+                                 uint32_t(byte_at(pos + 2)) << 16 | uint32_t(byte_at(pos + 3)) << 24;
+            node_off[u++] = pos;
+            maxdeg = std::max(maxdeg, deg);
+            pos += 4 + 10ull * deg;
+        }
+        unsigned char nt[4] = {};
+        for (int i = 0; i < 4; ++i) {
+            const int64_t x = (int64_t)ce - 4 + i;  // body offset of new tail byte i
+            if (x >= (int64_t)cs) nt[i] = h[x - (int64_t)cs];
+            else if (x >= 0) nt[i] = tail[4 - ((int64_t)cs - x)];
+        }
+        std::memcpy(tail, nt, 4);
+        cs = ce;
+    };
+    for (uint64_t off = 0; off < body; off += pin.bytes) {
+        const size_t bytes = (size_t)std::min<uint64_t>(pin.bytes, body - off);
+        fs.push_to(body_off + off, bytes, raw.p + off, walk);
+    }
+    if (u < idx->n || pos > body) fail(TSDG_ERUNTIME, tsdg_truncated_message(path, fs.size()));
+    node_off[idx->n] = pos;
+    idx->max_degree = maxdeg;
+    idx->R = std::max<uint32_t>(4, round_up(maxdeg, 4));
+    const size_t rows = std::max<uint32_t>(idx->n, 1);
+    cuda_check(cudaMalloc(&idx->adj, rows * idx->R * 4), "cudaMalloc(adj)");
+    cuda_check(cudaMalloc(&idx->lam, rows * idx->R * 2), "cudaMalloc(lam)");
+    cuda_check(cudaMalloc(&idx->deg_full, rows * 4), "cudaMalloc(deg)");
+    DevBuf<uint64_t> d_off(node_off.size(), idx->stream);
+    cuda_check(cudaMemcpyAsync(d_off.p, node_off.data(), node_off.size() * 8, cudaMemcpyHostToDevice,
+                               idx->stream),
+               "H2D node offsets");
+    if (idx->n) {
+        unpack_graph_kernel<<<decode_grid(idx), 256, 0, idx->stream>>>(
+            raw.p, d_off.p, 0, 0, idx->n, idx->n, idx->R, idx->adj, idx->lam, idx->deg_full, d_bad);
+        g_launches++;
+        cuda_check(cudaGetLastError(), "unpack_graph_kernel launch");
+    }
+    // node_off must outlive the async copy
+    cuda_check(cudaStreamSynchronize(idx->stream), "graph decode");
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* tsdg_gpu_last_error(void) { return g_err.c_str(); }
@@ -971,34 +1223,24 @@ int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint6
         if (metric < 0 || metric > 2) fail(TSDG_EINVAL, "invalid metric");
         if (n > 0 && (!base || !offsets || !targets || !lambdas))
             fail(TSDG_EINVAL, "index_create: null input array");
-        auto idx = std::make_unique<tsdg_gpu_index>();
-        idx->device = device;
-        DeviceGuard dg(device);
-        cudaDeviceProp prop{};
-        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-        idx->sm_count = prop.multiProcessorCount;
-        idx->n = n;
-        idx->d = d;
-        idx->ld = round_up(d, 4);
-        idx->metric = metric;
         uint32_t maxdeg = 0;
         for (uint32_t u = 0; u < n; ++u) {
             if (offsets[u + 1] < offsets[u]) fail(TSDG_EINVAL, "index_create: offsets not monotone");
             maxdeg = std::max<uint32_t>(maxdeg, (uint32_t)(offsets[u + 1] - offsets[u]));
         }
-        idx->max_degree = maxdeg;
-        idx->R = std::max<uint32_t>(4, round_up(maxdeg, 4));
         const uint64_t E = n ? offsets[n] : 0;
         for (uint64_t j = 0; j < E; ++j)
             if (targets[j] >= n) fail(TSDG_EINVAL, "index_create: edge target out of range");
-        cuda_check(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaStreamCreateWithFlags(&idx->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
-        // keep stream-ordered allocations cached across calls (no re-mapping per search)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
+        DeviceGuard dg(device);
+        IndexOwner own;
+        tsdg_gpu_index* idx = own.p;
+        idx->n = n;
+        idx->d = d;
+        idx->ld = round_up(d, 4);
+        idx->metric = metric;
+        idx->max_degree = maxdeg;
+        idx->R = std::max<uint32_t>(4, round_up(maxdeg, 4));
+        init_index_runtime(idx, device);
         // vectors, rows padded to ld floats (16-byte aligned for TMA bulk copies)
         const size_t nv = (size_t)std::max<uint32_t>(n, 1) * idx->ld;
         cuda_check(cudaMalloc(&idx->vec, nv * sizeof(float)), "cudaMalloc(vectors)");
@@ -1031,9 +1273,7 @@ int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint6
         cuda_check(cudaMemcpy(idx->lam, hlam.data(), na * 2, cudaMemcpyHostToDevice), "cudaMemcpy(lam)");
         cuda_check(cudaMemcpy(idx->deg_full, hdeg.data(), hdeg.size() * 4, cudaMemcpyHostToDevice),
                    "cudaMemcpy(deg)");
-        cuda_check(cudaMalloc(&idx->counters, kCounterSlots * 4), "cudaMalloc(counters)");
-        cuda_check(cudaMemset(idx->counters, 0, kCounterSlots * 4), "cudaMemset(counters)");
-        *out = idx.release();
+        *out = own.release();
     });
 }
 
@@ -1056,22 +1296,84 @@ int tsdg_gpu_index_create_from_file(const char* tsdg_path, const float* base, ui
                                  out);
 }
 
+int tsdg_gpu_index_create_from_files(const char* tsdg_path, const char* vectors_path, int device,
+                                     tsdg_gpu_index** out) {
+    return guarded([&] {
+        if (!out) fail(TSDG_EINVAL, "index_create_from_files: null out");
+        *out = nullptr;
+        if (!tsdg_path || !vectors_path) fail(TSDG_EINVAL, "index_create_from_files: null path");
+        const std::string gpath(tsdg_path), vpath(vectors_path);
+        // TSDG_LOAD_TRACE=1: phase times on stderr (development)
+        const bool trace = env_int("TSDG_LOAD_TRACE", 0) != 0;
+        auto t_last = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!trace) return;
+            const auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[load] %-16s %8.1f ms\n", what,
+                         std::chrono::duration<double, std::milli>(t - t_last).count());
+            t_last = t;
+        };
+        std::string err;
+        uint32_t vn = 0, vd = 0;
+        if (int rc = tsdg_vector_file_shape(vpath, &vn, &vd, err)) fail(rc, err);
+        // TSDG header (27 bytes; a shorter file fails in the parse with the
+        // reference-worded truncation message)
+        tsdg_graph_header h{};
+        uint64_t body_off = 0;
+        {
+            unsigned char hb[64] = {};
+            const int fd = open(gpath.c_str(), O_RDONLY);
+            if (fd < 0) fail(TSDG_ERUNTIME, gpath + ": cannot open for reading");
+            const ssize_t got = pread(fd, hb, sizeof(hb), 0);
+            close(fd);
+            if (got == 0) fail(TSDG_ERUNTIME, tsdg_truncated_message(gpath, 0));
+            if (got < 0) fail(TSDG_ERUNTIME, gpath + ": read failed");
+            if (int rc = tsdg_parse_header_bytes(gpath, hb, (size_t)got, &h, &body_off, err)) fail(rc, err);
+        }
+        mark("shape+header");
+        if (h.n != vn)
+            fail(TSDG_EINVAL, "index_create_from_files: graph has " + std::to_string(h.n) +
+                                  " nodes, base has " + std::to_string(vn));
+        if (h.metric > 2) fail(TSDG_EINVAL, "invalid metric");
+        DeviceGuard dg(device);
+        IndexOwner own;
+        tsdg_gpu_index* idx = own.p;
+        idx->n = vn;
+        idx->d = vd;
+        idx->ld = round_up(vd, 4);
+        idx->metric = h.metric;
+        init_index_runtime(idx, device);
+        mark("runtime");
+        const size_t rows = std::max<uint32_t>(vn, 1);
+        cuda_check(cudaMalloc(&idx->vec, rows * idx->ld * sizeof(float)), "cudaMalloc(vectors)");
+        DevBuf<unsigned long long> bad(2, idx->stream);
+        cuda_check(cudaMemsetAsync(bad.p, 0xFF, 2 * sizeof(unsigned long long), idx->stream), "memset");
+        PinnedPair pin(kStageChunk, idx->stream);
+        mark("alloc");
+        load_vectors_to_device(idx, vpath, pin, bad.p);
+        if (trace) cudaStreamSynchronize(idx->stream);
+        mark("vectors");
+        load_graph_to_device(idx, gpath, body_off, pin, bad.p + 1);
+        mark("graph");
+        unsigned long long hbad[2];
+        cuda_check(cudaMemcpyAsync(hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, idx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(idx->stream), "index_create_from_files");
+        if (hbad[0] != ~0ull) {
+            // the host parse reports the first bad record in the reference's wording
+            uint32_t pn = 0, pd = 0;
+            if (int rc = tsdg_parse_vector_file(vpath, nullptr, &pn, &pd, err)) fail(rc, err);
+            fail(TSDG_ERUNTIME, vpath + ": invalid record " + std::to_string(hbad[0]));
+        }
+        if (hbad[1] != ~0ull)
+            fail(TSDG_EINVAL, "index_create_from_files: edge target out of range at node " +
+                                  std::to_string(hbad[1]));
+        *out = own.release();
+    });
+}
+
 int tsdg_gpu_index_destroy(tsdg_gpu_index* idx) {
     return guarded([&] {
-        if (!idx) return;
-        DeviceGuard dg(idx->device);
-        cudaStreamSynchronize(idx->stream);
-        cudaStreamSynchronize(idx->stream2);
-        for (auto& kv : idx->degcut) cudaFree(kv.second);
-        if (idx->scratch) cudaFree(idx->scratch);
-        cudaFree(idx->vec);
-        cudaFree(idx->adj);
-        cudaFree(idx->lam);
-        cudaFree(idx->deg_full);
-        cudaFree(idx->counters);
-        cudaStreamDestroy(idx->stream);
-        cudaStreamDestroy(idx->stream2);
-        delete idx;
+        if (idx) free_index(idx);
     });
 }
 

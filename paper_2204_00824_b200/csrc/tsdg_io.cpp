@@ -10,9 +10,11 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/tsdg_gpu.h"
 
@@ -106,7 +108,197 @@ int parse_header(Reader& r, tsdg_graph_header& h) {
     return r.ok ? TSDG_OK : TSDG_ERUNTIME;
 }
 
+// open + mmap without the TSDG-specific size check (an empty vector file is the
+// reference's "empty dataset", not a truncation)
+int open_map_any(const std::string& path, Mapped& m, std::string& err) {
+    m.fd = open(path.c_str(), O_RDONLY);
+    if (m.fd < 0) {
+        err = path + ": cannot open for reading";
+        return TSDG_ERUNTIME;
+    }
+    struct stat st {};
+    if (fstat(m.fd, &st) != 0) {
+        err = path + ": cannot stat";
+        return TSDG_ERUNTIME;
+    }
+    m.size = static_cast<size_t>(st.st_size);
+    if (m.size == 0) return TSDG_OK;
+    void* p = mmap(nullptr, m.size, PROT_READ, MAP_PRIVATE, m.fd, 0);
+    if (p == MAP_FAILED) {
+        err = path + ": mmap failed";
+        m.size = 0;
+        return TSDG_ERUNTIME;
+    }
+    madvise(p, m.size, MADV_SEQUENTIAL);
+    m.p = static_cast<const unsigned char*>(p);
+    return TSDG_OK;
+}
+
+uint32_t le32(const unsigned char* p) {
+    return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+
+// fvecs / bvecs record stream (io.cpp:58-121): (int32-LE d, d components) repeated.
+// Walks the records in file order and reports the first error with the reference's
+// wording and byte offsets (io.cpp:27-33 truncation, :58-80 dimension checks,
+// :100-106 non-finite, :110 empty).  `out` (n x d floats) may be NULL; `n_out` /
+// `d_out` receive the record count and dimension.
+int parse_vector_records(const std::string& path, const unsigned char* p, size_t size,
+                         uint32_t comp_bytes, float* out, uint32_t* n_out, uint32_t* d_out,
+                         std::string& err) {
+    uint64_t off = 0;
+    uint32_t d = 0;
+    uint64_t index = 0;
+    while (off < size) {
+        const uint64_t rec_off = off;
+        if (size - off < 4) {
+            err = path + ": truncated file while reading record dimension at byte offset " +
+                  std::to_string(off);
+            return TSDG_ERUNTIME;
+        }
+        const int32_t rd = static_cast<int32_t>(le32(p + off));
+        off += 4;
+        const std::string where = " at record " + std::to_string(index) + " (byte offset " +
+                                  std::to_string(rec_off) + ")";
+        if (rd > (1 << 24)) {
+            err = path + ": implausible dimension " + std::to_string(rd) + where;
+            return TSDG_ERUNTIME;
+        }
+        if (rd <= 0) {
+            err = path + ": invalid dimension " + std::to_string(rd) + where;
+            return TSDG_ERUNTIME;
+        }
+        if (d != 0 && static_cast<uint32_t>(rd) != d) {
+            err = path + ": inconsistent dimension at record " + std::to_string(index) +
+                  " (byte offset " + std::to_string(rec_off) + "): got " + std::to_string(rd) +
+                  ", expected " + std::to_string(d);
+            return TSDG_ERUNTIME;
+        }
+        if (d == 0) d = static_cast<uint32_t>(rd);
+        const uint64_t body = static_cast<uint64_t>(comp_bytes) * d;
+        if (size - off < body) {
+            err = path + ": truncated file while reading record components at byte offset " +
+                  std::to_string(off);
+            return TSDG_ERUNTIME;
+        }
+        for (uint32_t j = 0; j < d; ++j) {
+            float v;
+            if (comp_bytes == 1) {
+                v = static_cast<float>(p[off + j]);
+            } else {
+                const uint32_t b = le32(p + off + 4ull * j);
+                std::memcpy(&v, &b, 4);
+            }
+            if (!std::isfinite(v)) {
+                err = path + ": non-finite value at record " + std::to_string(index) +
+                      " component " + std::to_string(j) + " (byte offset " +
+                      std::to_string(rec_off + 4 + static_cast<uint64_t>(comp_bytes) * j) + ")";
+                return TSDG_ERUNTIME;
+            }
+            if (out) out[index * d + j] = v;
+        }
+        off += body;
+        ++index;
+    }
+    if (index == 0) {
+        err = path + ": empty dataset";
+        return TSDG_ERUNTIME;
+    }
+    if (n_out) *n_out = static_cast<uint32_t>(index);
+    if (d_out) *d_out = d;
+    return TSDG_OK;
+}
+
+bool ends_with(const std::string& s, const char* suf) {
+    const size_t k = std::strlen(suf);
+    return s.size() >= k && s.compare(s.size() - k, k, suf) == 0;
+}
+
 }  // namespace
+
+// io.cpp:112-117: .bvecs -> uint8 components, anything else -> float32.
+uint32_t tsdg_vector_component_bytes(const std::string& path) { return ends_with(path, ".bvecs") ? 1 : 4; }
+
+// Shape of a vector file from its first record and its size: records are
+// fixed-size once the first dimension is known.  Returns TSDG_OK and (n, d) when
+// the size is an exact multiple of the record size and the first record's
+// dimension is valid; otherwise runs the full parse so the error names the first
+// bad record exactly as the reference does.  Record headers past the first and
+// component values are NOT checked here (the device unpack checks them).
+int tsdg_vector_file_shape(const std::string& path, uint32_t* n, uint32_t* d, std::string& err) {
+    Mapped m;
+    if (int rc = open_map_any(path, m, err)) return rc;
+    const uint32_t cb = tsdg_vector_component_bytes(path);
+    if (m.size >= 4) {
+        const int32_t rd = static_cast<int32_t>(le32(m.p));
+        if (rd > 0 && rd <= (1 << 24)) {
+            const uint64_t rec = 4 + static_cast<uint64_t>(cb) * rd;
+            if (m.size % rec == 0 && m.size / rec <= 0xFFFFFFFFull) {
+                *n = static_cast<uint32_t>(m.size / rec);
+                *d = static_cast<uint32_t>(rd);
+                return TSDG_OK;
+            }
+        }
+    }
+    return parse_vector_records(path, m.p, m.size, cb, nullptr, n, d, err);
+}
+
+// Full host parse (the error path of the device loader; also the host loader).
+int tsdg_parse_vector_file(const std::string& path, float* out, uint32_t* n, uint32_t* d,
+                           std::string& err) {
+    Mapped m;
+    if (int rc = open_map_any(path, m, err)) return rc;
+    return parse_vector_records(path, m.p, m.size, tsdg_vector_component_bytes(path), out, n, d,
+                                err);
+}
+
+// TSDG header from its first bytes (the streaming loader reads the body itself).
+int tsdg_parse_header_bytes(const std::string& path, const unsigned char* p, size_t size,
+                            tsdg_graph_header* h, uint64_t* body_off, std::string& err) {
+    Reader r{path, p, size};
+    if (int rc = parse_header(r, *h)) {
+        err = r.err;
+        return rc;
+    }
+    *body_off = r.off;
+    return TSDG_OK;
+}
+
+// The reference-worded truncation message of the bulk reader (for a TSDG whose
+// node records run past the end of the file).
+std::string tsdg_truncated_message(const std::string& path, uint64_t file_size) {
+    return path + ": truncated file at byte offset " + std::to_string(file_size);
+}
+
+extern "C" int tsdg_read_vectors_shape(const char* path, uint32_t* n, uint32_t* d) {
+    if (!path || !n || !d) {
+        tsdg_set_error("read_vectors_shape: null argument");
+        return TSDG_EINVAL;
+    }
+    std::string err;
+    const int rc = tsdg_vector_file_shape(path, n, d, err);
+    if (rc) tsdg_set_error(err);
+    return rc;
+}
+
+extern "C" int tsdg_read_vectors(const char* path, float* out, uint32_t n, uint32_t d) {
+    if (!path || !out) {
+        tsdg_set_error("read_vectors: null argument");
+        return TSDG_EINVAL;
+    }
+    std::string err;
+    uint32_t fn = 0, fd = 0;
+    int rc = tsdg_vector_file_shape(path, &fn, &fd, err);
+    if (!rc && (fn != n || fd != d)) {
+        tsdg_set_error(std::string(path) + ": file holds " + std::to_string(fn) + " x " +
+                       std::to_string(fd) + " vectors, caller expects " + std::to_string(n) +
+                       " x " + std::to_string(d));
+        return TSDG_EINVAL;
+    }
+    if (!rc) rc = tsdg_parse_vector_file(path, out, &fn, &fd, err);
+    if (rc) tsdg_set_error(err);
+    return rc;
+}
 
 extern "C" int tsdg_read_tsdg_header(const char* path_c, tsdg_graph_header* out) {
     if (!path_c || !out) {

@@ -126,6 +126,16 @@ def load_tsdg(path: str) -> TsdgGraph:
                      lam, dst, int(h.max_degree))
 
 
+def read_vectors(path: str) -> np.ndarray:
+    """fvecs / bvecs file -> (n, d) float32 (tsdg::load_vectors, io.cpp:112-117;
+    bvecs components widened to float).  Errors carry the reference's messages."""
+    n, d = ctypes.c_uint32(), ctypes.c_uint32()
+    check(lib().tsdg_read_vectors_shape(path.encode(), ctypes.byref(n), ctypes.byref(d)))
+    out = np.empty((n.value, d.value), np.float32)
+    check(lib().tsdg_read_vectors(path.encode(), _p(out), n.value, d.value))
+    return out
+
+
 def _f32rows(a, d: Optional[int] = None) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float32)
     if a.ndim == 1:
@@ -153,14 +163,33 @@ class GpuIndex:
             _p(np.ascontiguousarray(graph.lambdas, np.uint16)), int(graph.metric), device,
             ctypes.byref(h)))
         self._h = h
-        info = [ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_int(), ctypes.c_uint32(),
-                ctypes.c_int(), ctypes.c_uint32(), ctypes.c_uint32()]
-        check(lib().tsdg_gpu_index_info(self._h, *[ctypes.byref(x) for x in info]))
-        self.max_degree, self.row_stride, self.adj_stride = info[3].value, info[5].value, info[6].value
+        self._read_info()
 
     @classmethod
     def from_file(cls, tsdg_path: str, base, device: int = 0) -> "GpuIndex":
         return cls(load_tsdg(tsdg_path), base, device)
+
+    @classmethod
+    def from_files(cls, tsdg_path: str, vectors_path: str, device: int = 0) -> "GpuIndex":
+        """Index straight from a reference .tsdg file and an fvecs/bvecs base: the
+        raw file bytes are decoded on the device (tsdg_gpu_index_create_from_files);
+        no host graph or vector array is built."""
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        check(lib().tsdg_gpu_index_create_from_files(tsdg_path.encode(), vectors_path.encode(),
+                                                     device, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.graph = None
+        self._read_info()
+        return self
+
+    def _read_info(self) -> None:
+        info = [ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_int(), ctypes.c_uint32(),
+                ctypes.c_int(), ctypes.c_uint32(), ctypes.c_uint32()]
+        check(lib().tsdg_gpu_index_info(self._h, *[ctypes.byref(x) for x in info]))
+        self.n, self.d, self.metric = info[0].value, info[1].value, info[2].value
+        self.max_degree, self.row_stride, self.adj_stride = info[3].value, info[5].value, info[6].value
 
     def close(self) -> None:
         if getattr(self, "_h", None):

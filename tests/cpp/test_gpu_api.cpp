@@ -14,6 +14,7 @@
 #include "tsdg/bench.hpp"
 #include "tsdg/bestfirst_search.hpp"
 #include "tsdg/greedy_search.hpp"
+#include "tsdg/io.hpp"
 #include "tsdg/knn_graph.hpp"
 #include "tsdg/reference.hpp"
 #include "tsdg/gpu_search.hpp"
@@ -239,6 +240,34 @@ int main() {
         CHECK(same);
         std::remove(paths[0].c_str());
         std::remove(paths[1].c_str());
+    }
+    {
+        CASE("Index(tsdg file, fvecs file) decoded on the device == load_tsdg + load_vectors");
+        auto [base, queries] = make_synthetic_split(2500, 60, 20, 5, 0.25f, 91);
+        const TsdgGraph g = build(base, brute_force_knn(base, 24, Metric::L2), {1.2f, 9, 0}, Metric::L2);
+        const std::string gp = "/tmp/tsdg_files_case.tsdg", vp = "/tmp/tsdg_files_case.fvecs";
+        save_tsdg(g, gp);
+        write_fvecs(base, vp);
+        const gpu::Index from_files(gp, vp);
+        const gpu::Index from_memory(load_tsdg(gp), load_vectors(vp));
+        BestFirstParams p;
+        p.k = 12;
+        p.seed = 4;
+        SearchStats s_a, s_b;
+        CHECK(from_files.large_batch_search(queries, p, &s_a) == large_batch_search(g, base, queries, p, &s_b));
+        CHECK(s_a.distance_evals == s_b.distance_evals && s_a.hops == s_b.hops);
+        GreedyParams gp2;
+        gp2.t0 = 4;
+        CHECK(from_files.small_batch_search(queries, 10, gp2) == from_memory.small_batch_search(queries, 10, gp2));
+        bool threw = false;
+        try {
+            const gpu::Index bad(gp, "/tmp/tsdg_files_case_missing.fvecs");
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()).find("cannot open for reading") != std::string::npos;
+        }
+        CHECK(threw);
+        std::remove(gp.c_str());
+        std::remove(vp.c_str());
     }
     std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;
