@@ -69,6 +69,42 @@ def test_bestfirst_random_params(orc, fixtures, index, name):
         assert_same(idx.search_bestfirst(q, p), orc.large_batch(g, b, q, p))
 
 
+@pytest.mark.parametrize("name", FIXTURES)
+def test_bestfirst_maximum_k(orc, fixtures, index, name):
+    """The largest result sizes the GPU path accepts (k up to 1024, R in shared
+    memory) with heavy queue overflow (m = 1 / 8 / 32): still bit-exact, counters
+    included (queue_evictions large)."""
+    g, b, q = fixtures(name)
+    idx = index(name)
+    q = q[:48]
+    evictions = 0
+    for k, m, cut in ((128, 8, 10), (512, 32, 12), (1024, 32, 12), (300, 1, 5)):
+        p = BestFirstParams(k=k, m_segments=m, lambda_cut=cut, seed=k + m)
+        got, want = idx.search_bestfirst(q, p), orc.large_batch(g, b, q, p)
+        assert_same(got, want)
+        evictions += int(want.stats[:, 2].sum())
+    assert evictions > 0
+    with pytest.raises(InvalidArgument):
+        idx.search_bestfirst(q, BestFirstParams(k=1025))
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_greedy_maximum_t0_and_k(orc, fixtures, index, name):
+    """Alg. 1 at the GPU path's limits: t0 = 256 walks (global-memory pool + merge
+    kernel) with k up to 32 * t0, and t0 = 16 / 17 on both sides of the cluster
+    limit; bit-exact ids, distances, counts and counters."""
+    g, b, q = fixtures(name)
+    idx = index(name)
+    q = q[:16]
+    for t0, k, T, cut in ((256, 2000, 16, 10), (256, 8192, 4, 3), (17, 100, 16, 10),
+                          (16, 512, 16, 10)):
+        p = GreedyParams(t0=t0, hop_limit=T, lambda_cut=cut, seed=t0 * 7 + k)
+        got, want = idx.search_greedy(q, k, p), orc.small_batch(g, b, q, k, p)
+        assert_same(got, want)
+    with pytest.raises(InvalidArgument):
+        idx.search_greedy(q, 10, GreedyParams(t0=257))
+
+
 def test_bestfirst_query_index_base_split(orc, fixtures, index):
     g, b, q = fixtures("syn2k")
     idx = index("syn2k")
