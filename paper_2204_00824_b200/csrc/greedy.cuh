@@ -9,7 +9,7 @@
 //     per-lane minimum of lane_update (rank_list.cpp:8-18) in registers;
 //   - merge_halves (rank_list.cpp:20-49) as a warp operation: bitonic sort of
 //     R_temp, id-dedup of its best 16 finite entries against R_ij by shuffles,
-//     then a 64-key bitonic sort of (R_ij, newcomers) keeping the first 32;
+//     then a bitonic merge of R_ij with the reversed new entries (6 steps);
 //   - u <- closest of R_temp (not R_ij); stop when the merge changed nothing.
 // Rows are staged with the same TMA bulk-copy gather as the best-first kernel,
 // so distances are the reference's sequential fp32 values bit for bit.
@@ -44,67 +44,44 @@ struct GrArgs {
     uint32_t warp_smem, off_query, off_stage, off_bar;
 };
 
-// Ascending bitonic sort of 64 keys: (da,ia) is index lane, (db,ib) index 32+lane.
-__device__ __forceinline__ void warp_sort64(float& da, uint32_t& ia, float& db, uint32_t& ib,
-                                            int lane) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {  // only at k == 64: ascending, a keeps min
-                const bool b_first = closer(db, ib, da, ia);
-                if (b_first) {
-                    const float td = da;
-                    const uint32_t ti = ia;
-                    da = db;
-                    ia = ib;
-                    db = td;
-                    ib = ti;
-                }
-            } else {
-                const float oda = __shfl_xor_sync(kFull, da, j);
-                const uint32_t oia = __shfl_xor_sync(kFull, ia, j);
-                const float odb = __shfl_xor_sync(kFull, db, j);
-                const uint32_t oib = __shfl_xor_sync(kFull, ib, j);
-                const bool lower = (lane & j) == 0;
-                const bool up_a = (lane & k) == 0;
-                const bool up_b = ((lane + 32) & k) == 0;
-                cx(da, ia, oda, oia, lower == up_a);
-                cx(db, ib, odb, oib, lower == up_b);
-            }
-        }
-    }
-}
-
 // merge_halves (rank_list.cpp:20-49).  (rd, ri): R_ij slot `lane` (sorted);
 // (td, ti): R_temp slot `lane`.  Returns the warp-uniform "updated".
+//
+// The reference pools R_ij with the best 16 finite newcomers, keeping the closer
+// copy of a repeated id, sorts the pool and keeps 32.  A repeated id always carries
+// the same distance (a pure function of the query and the node), so "keep the
+// closer copy" never replaces anything: the pool is R_ij plus the newcomers whose
+// id is new.  Both parts are already sorted (R_ij by contract, the newcomers as a
+// subsequence of the sorted R_temp), so instead of sorting 64 keys the warp forms
+// the bitonic sequence R_ij ++ reverse(newcomers), keeps the lower half of one
+// half-cleaner step (the 32 smallest) and sorts it with 5 more steps.
 __device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float td,
                                                   uint32_t ti, int lane) {
-    const float kInf = __int_as_float(0x7f800000);
     warp_sort32(td, ti, lane);  // incoming, ascending
-    const bool cand = lane < 16 && ti != kInvalid;
-    int found = -1;
+    // repeated ids: against R_ij, and within the newcomers (adjacent once sorted)
+    const uint32_t prev = __shfl_up_sync(kFull, ti, 1);
+    bool dup = lane > 0 && prev == ti;
 #pragma unroll 8
-    for (int t = 0; t < 32; ++t) {
-        const uint32_t oi = __shfl_sync(kFull, ri, t);
-        if (cand && found < 0 && oi == ti) found = t;
-    }
-    // in-place replacement when the newcomer is closer than its duplicate
+    for (int t = 0; t < 32; ++t) dup |= __shfl_sync(kFull, ri, t) == ti;
+    const unsigned vm = __ballot_sync(kFull, lane < 16 && ti != kInvalid && !dup);
+    // lane L takes newcomer number 31 - L (the reversed, compacted newcomer list)
+    const uint32_t want = 31u - (uint32_t)lane;
+    const bool has = want < (uint32_t)__popc(vm);
+    const int src = has ? (int)__fns(vm, 0, (int)want + 1) : 0;
+    const float sd = __shfl_sync(kFull, td, src);
+    const uint32_t sid = __shfl_sync(kFull, ti, src);
     float nd = rd;
     uint32_t ni = ri;
-#pragma unroll 4
-    for (int src = 0; src < 16; ++src) {
-        const int f = __shfl_sync(kFull, found, src);
-        const float sd = __shfl_sync(kFull, td, src);
-        const uint32_t sid = __shfl_sync(kFull, ti, src);
-        if (f == lane && closer(sd, sid, nd, ni)) {
-            nd = sd;
-            ni = sid;
-        }
+    if (has && closer(sd, sid, nd, ni)) {  // half-cleaner: lower half keeps the min
+        nd = sd;
+        ni = sid;
     }
-    float bd = (cand && found < 0) ? td : kInf;
-    uint32_t bi = (cand && found < 0) ? ti : kInvalid;
-    warp_sort64(nd, ni, bd, bi, lane);
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const float od = __shfl_xor_sync(kFull, nd, j);
+        const uint32_t oi = __shfl_xor_sync(kFull, ni, j);
+        cx(nd, ni, od, oi, (lane & j) == 0);
+    }
     const bool changed = (nd != rd) || (ni != ri);
     rd = nd;
     ri = ni;
