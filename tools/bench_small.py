@@ -11,7 +11,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle.oracle import recall_at_k  # noqa: E402  (checker only)
+from bench import recall_at_k  # noqa: E402  (bench.cpp:59-78, vectorised)
 from paper_2204_00824_b200 import _native, datasets  # noqa: E402
 from paper_2204_00824_b200.search import GpuIndex, GreedyParams, load_tsdg  # noqa: E402
 
