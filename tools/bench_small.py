@@ -60,3 +60,26 @@ if __name__ == "__main__":
                 r["kernel"] = kern
                 r["mode"] = "fast" if mode else "det"
                 print(json.dumps(r), flush=True)
+    if os.environ.get("REF") == "1":
+        # reference arm (as bench.py --impl reference): the unmodified reference's
+        # small_batch_search on the host cores, wall clock per call, same batches
+        import time
+        from oracle import oracle as O
+        ref = O.Ref()
+        fx = ref.fixture(ds.graph_path, ds.base)
+        for t0 in [int(x) for x in os.environ.get("T0S", "8,16").split(",")]:
+            p = GreedyParams(t0=t0, seed=7)
+            for batch in (1, 8, 64):
+                reps = max(4, min(64, 512 // batch))
+                fx.small_batch(ds.queries[:batch], 10, p)
+                ts = []
+                for i in range(reps):
+                    q = ds.queries[i * batch:(i + 1) * batch]
+                    t = time.perf_counter()
+                    fx.small_batch(q, 10, p)
+                    ts.append((time.perf_counter() - t) * 1e3)
+                lat = float(np.median(ts))
+                print(json.dumps({"batch": batch, "t0": t0, "latency_ms_p50": lat,
+                                  "qps": batch / lat * 1e3, "impl": "reference_cpu",
+                                  "threads": ref.so.ref_num_threads(), "queries": reps * batch}),
+                      flush=True)
