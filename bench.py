@@ -15,7 +15,9 @@ ours:      `value` = device-resident throughput (queries already in HBM; CUDA ev
            on the launching stream around each step; L2 flushed between steps);
            `e2e`   = same search through the reference-facing C-ABI call with HOST
            buffers (pinned), H2D of the queries and D2H of ids/dists/counts inside
-           the timed region.
+           the timed region (pinned buffers take the zero-copy path: the kernel
+           reads each query from host memory and writes its results back over the
+           bus while the search runs; TSDG_ZERO_COPY=0 selects the copy pipeline).
 reference: the reference's own CPU large_batch_search (oracle/_ref, unmodified,
            OpenMP on all host cores) on the same config.
 Multi-GPU (torchrun, one process per GPU): the index is replicated; each rank
@@ -579,7 +581,9 @@ def main():
                          "edges_per_query": head["examined"] / nq},
             "e2e": {"value": e2e_val, "unit": "queries/s",
                     "h2d_bytes_per_step": int(ds.queries.nbytes),
-                    "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
+                    "d2h_bytes_per_step": int(nq * k * 8 + nq * 4),
+                    "transfer": "zero-copy (kernel reads/writes pinned host memory)"
+                    if os.environ.get("TSDG_ZERO_COPY", "1") != "0" else "copy pipeline (2 chunks, 2 streams)"},
             "gpu_launches": head["launches"],
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -954,6 +954,26 @@ void run_per_device(size_t ndev, F&& fn) {
     for (size_t i = 0; i < ndev; ++i)
         if (rc[i] != TSDG_OK) fail(rc[i], msg[i]);
 }
+// Device alias of a host buffer [p, p + bytes) when it lies in one mapped pinned
+// allocation (cudaHostAlloc / cudaMallocHost / registered-mapped memory, e.g. torch
+// pin_memory()); nullptr otherwise (pageable memory: the copy pipeline is used).
+template <class T>
+T* mapped_alias(T* p, size_t bytes) {
+    if (!p || bytes == 0) return nullptr;
+    cudaPointerAttributes a{}, b{};
+    const char* last = reinterpret_cast<const char*>(p) + bytes - 1;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess || cudaPointerGetAttributes(&b, last) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || !a.devicePointer || !b.devicePointer)
+        return nullptr;
+    if (static_cast<const char*>(b.devicePointer) - static_cast<const char*>(a.devicePointer) !=
+        static_cast<ptrdiff_t>(bytes - 1))
+        return nullptr;
+    return static_cast<T*>(a.devicePointer);
+}
+
 // contiguous slice [begin, end) of nq for part i of ndev
 void slice_of(uint32_t nq, size_t ndev, size_t i, uint32_t& b, uint32_t& e) {
     b = (uint32_t)((uint64_t)nq * i / ndev);
@@ -1438,6 +1458,23 @@ int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_
         std::lock_guard<std::mutex> lk(idx->mu);
         DeviceGuard dg(idx->device);
         const uint32_t k = params->k;
+        // Zero-copy when every buffer is mapped pinned host memory (TSDG_ZERO_COPY=0
+        // disables): the kernel reads each query from host memory once (into shared
+        // memory) and writes its results straight back over the bus, so the upload
+        // and download overlap the whole search instead of bracketing it.
+        if (env_int("TSDG_ZERO_COPY", 1)) {
+            const float* zq = mapped_alias(queries, (size_t)nq * idx->d * 4);
+            uint32_t* zi = mapped_alias(ids, (size_t)nq * k * 4);
+            float* zd = mapped_alias(dists, (size_t)nq * k * 4);
+            uint32_t* zc = mapped_alias(counts, (size_t)nq * 4);
+            tsdg_query_stats* zs = mapped_alias(stats, (size_t)nq * sizeof(tsdg_query_stats));
+            if (zq && zi && (zd || !dists) && (zc || !counts) && (zs || !stats)) {
+                launch_bestfirst(idx, zq, nq, query_index_base, params, mode, zi, zd, zc, zs,
+                                 idx->stream);
+                cuda_check(cudaStreamSynchronize(idx->stream), "bestfirst_search");
+                return;
+            }
+        }
         // grow-only scratch: queries | ids | dists | counts | stats
         const size_t bq = (size_t)nq * idx->d * 4, bi = (size_t)nq * k * 4, bc = (size_t)nq * 4,
                      bs = (size_t)nq * sizeof(tsdg_query_stats);

@@ -175,3 +175,35 @@ def test_multi_device_index_equals_single(fixtures, index):
     _same(multi.search_greedy(q, 10, gp), idx.search_greedy(q, 10, gp))
     _same(multi.search_bestfirst(q[:2], p), idx.search_bestfirst(q[:2], p))  # fewer queries than devices
     multi.close()
+
+
+def test_zero_copy_host_path_equals_copy_pipeline(fixtures, index, monkeypatch):
+    """Pinned host buffers take the zero-copy path (the kernel reads queries from and
+    writes results to mapped host memory); pageable ones the copy pipeline.  Both
+    equal the device-pointer search, ids, distances, counts and counters."""
+    import ctypes
+    import torch
+    from paper_2204_00824_b200.search import BestFirstParams
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    p = BestFirstParams(k=12, seed=9)
+    want = idx.search_bestfirst(q, p)  # pageable numpy buffers: copy pipeline
+    nq, k = q.shape[0], p.k
+    hq = torch.from_numpy(np.ascontiguousarray(q)).pin_memory()
+    hi = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    hd = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    hc = torch.empty(nq, dtype=torch.int32).pin_memory()
+    hs = torch.empty((nq, 4), dtype=torch.int32).pin_memory()
+    pc = p.c()
+    L = _native.lib()
+    for zc in ("1", "0"):
+        monkeypatch.setenv("TSDG_ZERO_COPY", zc)
+        hi.fill_(-7)
+        _native.check(L.tsdg_gpu_search_bestfirst(
+            idx.handle, ctypes.c_void_p(hq.data_ptr()), nq, 0, ctypes.byref(pc), _native.MODE_DETERMINISTIC,
+            ctypes.c_void_p(hi.data_ptr()), ctypes.c_void_p(hd.data_ptr()), ctypes.c_void_p(hc.data_ptr()),
+            ctypes.c_void_p(hs.data_ptr())))
+        np.testing.assert_array_equal(hi.numpy().view(np.uint32), want.ids)
+        np.testing.assert_array_equal(hd.numpy().view(np.uint32), want.dists.view(np.uint32))
+        np.testing.assert_array_equal(hc.numpy().view(np.uint32), want.counts)
+        np.testing.assert_array_equal(hs.numpy()[:, 1].view(np.uint32), want.stats["distance_evals"])
