@@ -1574,6 +1574,20 @@ int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t n
         std::lock_guard<std::mutex> lk(idx->mu);
         DeviceGuard dg(idx->device);
         cudaStream_t st = idx->stream;
+        // zero-copy with mapped pinned buffers (see tsdg_gpu_search_bestfirst): at
+        // small batch this removes two copy round trips from the call's latency
+        if (env_int("TSDG_ZERO_COPY", 1)) {
+            const float* zq = mapped_alias(queries, (size_t)nq * idx->d * 4);
+            uint32_t* zi = mapped_alias(ids, (size_t)nq * k * 4);
+            float* zd = mapped_alias(dists, (size_t)nq * k * 4);
+            uint32_t* zc = mapped_alias(counts, (size_t)nq * 4);
+            tsdg_query_stats* zs = mapped_alias(stats, (size_t)nq * sizeof(tsdg_query_stats));
+            if (zq && zi && (zd || !dists) && (zc || !counts) && (zs || !stats)) {
+                launch_greedy(idx, zq, nq, k, params, mode, zi, zd, zc, zs, st);
+                cuda_check(cudaStreamSynchronize(st), "small_batch_search");
+                return;
+            }
+        }
         float* dq = dev_alloc<float>((size_t)nq * idx->d, st);
         uint32_t* di = dev_alloc<uint32_t>((size_t)nq * k, st);
         float* dd = dev_alloc<float>((size_t)nq * k, st);

@@ -207,3 +207,30 @@ def test_zero_copy_host_path_equals_copy_pipeline(fixtures, index, monkeypatch):
         np.testing.assert_array_equal(hd.numpy().view(np.uint32), want.dists.view(np.uint32))
         np.testing.assert_array_equal(hc.numpy().view(np.uint32), want.counts)
         np.testing.assert_array_equal(hs.numpy()[:, 1].view(np.uint32), want.stats["distance_evals"])
+
+
+def test_zero_copy_greedy_equals_copy_path(fixtures, index, monkeypatch):
+    """Small batch through the host-pointer call: pinned buffers (zero-copy) and
+    pageable buffers give identical results, for the cluster and the warp kernel."""
+    import ctypes
+    import torch
+    from paper_2204_00824_b200.search import GreedyParams
+    _, _, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    L = _native.lib()
+    for nq, t0 in ((1, 16), (8, 8), (200, 16)):
+        qq = np.ascontiguousarray(q[:nq])
+        p = GreedyParams(t0=t0, seed=3)
+        want = idx.search_greedy(qq, 10, p)
+        hq = torch.from_numpy(qq).pin_memory()
+        hi = torch.full((nq, 10), -7, dtype=torch.int32).pin_memory()
+        hd = torch.empty((nq, 10), dtype=torch.float32).pin_memory()
+        hc = torch.empty(nq, dtype=torch.int32).pin_memory()
+        pc = p.c()
+        _native.check(L.tsdg_gpu_search_greedy(
+            idx.handle, ctypes.c_void_p(hq.data_ptr()), nq, 10, ctypes.byref(pc), _native.MODE_DETERMINISTIC,
+            ctypes.c_void_p(hi.data_ptr()), ctypes.c_void_p(hd.data_ptr()), ctypes.c_void_p(hc.data_ptr()),
+            None))
+        np.testing.assert_array_equal(hi.numpy().view(np.uint32), want.ids)
+        np.testing.assert_array_equal(hd.numpy().view(np.uint32), want.dists.view(np.uint32))
+        np.testing.assert_array_equal(hc.numpy().view(np.uint32), want.counts)
