@@ -139,7 +139,11 @@ int tsdg_gpu_deg_cut(tsdg_gpu_index* idx, uint32_t lambda_cut, uint32_t* out);
  * the stream Rng64(params.seed).fork(query_index_base + q); with base 0 this is the
  * reference batch call, and a split batch (multi-GPU) passes its slice start.
  * ids: nq x k, ascending by (dist, id), padded 0xFFFFFFFF; dists padded +inf;
- * counts: nq; stats: nq entries or NULL.  HOST pointers; all copies inside. */
+ * counts: nq; stats: nq entries or NULL.  HOST pointers; all transfers inside the
+ * call: when every buffer lies in mapped pinned memory (cudaMallocHost /
+ * cudaHostAlloc / torch pin_memory) the kernel reads the queries and writes the
+ * results over the bus directly (zero-copy); otherwise a copy/compute pipeline.
+ * TSDG_ZERO_COPY=0 forces the pipeline.  Same results either way. */
 int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
                               uint64_t query_index_base, const tsdg_bf_params* params,
                               int mode, uint32_t* ids, float* dists, uint32_t* counts,
@@ -154,7 +158,8 @@ int tsdg_gpu_search_bestfirst_device(tsdg_gpu_index* idx, const float* d_queries
 /* ---- small batch: multi-start greedy, Alg. 1 --------------------------------
  * Replaces tsdg::small_batch_search (greedy_search.cpp:106-127): t0 walks per query
  * with streams Rng64(seed).fork(s) (the same for every query), merged by
- * (dist, id) with id-dedup, first k.  Output layout as for best-first. */
+ * (dist, id) with id-dedup, first k.  Output layout as for best-first; HOST
+ * pointers, zero-copy with mapped pinned buffers as for best-first. */
 int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t nq, uint32_t k,
                            const tsdg_greedy_params* params, int mode, uint32_t* ids,
                            float* dists, uint32_t* counts, tsdg_query_stats* stats);
