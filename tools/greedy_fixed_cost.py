@@ -16,7 +16,7 @@ from paper_2204_00824_b200.search import GpuIndex, GreedyParams, load_tsdg  # no
 
 ds = datasets.load("c2_lowlid_1m")
 idx = GpuIndex(load_tsdg(ds.graph_path), ds.base)
-os.environ["TSDG_GREEDY"] = "cta"
+os.environ.setdefault("TSDG_GREEDY", "cta")
 dq = torch.from_numpy(ds.queries[:256]).cuda()
 ids = torch.empty((256, 10), dtype=torch.int32, device="cuda")
 dd = torch.empty((256, 10), dtype=torch.float32, device="cuda")
