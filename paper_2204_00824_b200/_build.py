@@ -31,27 +31,41 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_gpu(force: bool = False) -> str:
+GPU_SRCS = ("tsdg_gpu.cu", "bf_fast.cu", "tsdg_io.cpp")
+
+
+def _build_so(out: str, extra: list, force: bool) -> str:
+    """Compile every translation unit to an object in parallel, then link."""
     os.makedirs(LIB, exist_ok=True)
-    out = os.path.join(LIB, "libtsdg_gpu.so")
-    srcs = [os.path.join(CSRC, f) for f in ("tsdg_gpu.cu", "tsdg_io.cpp")]
+    srcs = [os.path.join(CSRC, f) for f in GPU_SRCS]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     deps.append(os.path.join(ROOT, "include", "tsdg_gpu.h"))
-    if force or _stale(out, deps):
-        _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-              "-shared", "-o", out, *srcs])
+    if not (force or _stale(out, deps)):
+        return out
+    objdir = os.path.join(LIB, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    tag = os.path.splitext(os.path.basename(out))[0]
+    objs, procs = [], []
+    for src in srcs:
+        obj = os.path.join(objdir, f"{tag}.{os.path.basename(src)}.o")
+        cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", *extra, "-Xcompiler", "-fPIC,-O2",
+               "-c", "-o", obj, src]
+        print("[build]", " ".join(cmd), flush=True)
+        procs.append(subprocess.Popen(cmd, cwd=ROOT))
+        objs.append(obj)
+    if any(p.wait() != 0 for p in procs):
+        raise RuntimeError(f"nvcc failed building {out}")
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs])
     return out
+
+
+def build_gpu(force: bool = False) -> str:
+    return _build_so(os.path.join(LIB, "libtsdg_gpu.so"), [], force)
 
 
 def build_gpu_phases(force: bool = False) -> str:
     """Development variant with per-phase clock64 counters (-DTSDG_PHASES)."""
-    out = os.path.join(LIB, "libtsdg_gpu_phases.so")
-    srcs = [os.path.join(CSRC, f) for f in ("tsdg_gpu.cu", "tsdg_io.cpp")]
-    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
-    if force or _stale(out, deps):
-        _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-DTSDG_PHASES", "-Xcompiler",
-              "-fPIC,-O2", "-shared", "-o", out, *srcs])
-    return out
+    return _build_so(os.path.join(LIB, "libtsdg_gpu_phases.so"), ["-DTSDG_PHASES"], force)
 
 
 def build_datagen(force: bool = False) -> str:

@@ -61,6 +61,7 @@ struct BfArgs {
     // per-warp shared-memory carve (bytes)
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
         off_vsize, off_voldest, off_rid, off_rdist, off_bar, off_rowid;
+    uint32_t off_lst, off_dl;  // bf_fast_kernel: needed-row ids / distances (64 + pad)
 };
 
 struct BfWarp {

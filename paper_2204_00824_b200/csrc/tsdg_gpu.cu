@@ -29,6 +29,7 @@
 #include "../../include/tsdg_gpu.h"
 #include <cub/device/device_scan.cuh>
 
+#include "bf_fast.cuh"
 #include "diversify.cuh"
 #include "exact_scan.cuh"
 #include "greedy_cluster.cuh"
@@ -268,6 +269,19 @@ BfKernel pick_bf(int metric, bool fast, bool tma, bool kreg) {
     return fast ? pick_bf<2, true>(tma, kreg) : pick_bf<2, false>(tma, kreg);
 }
 
+// bf_fast_kernel per-warp carve: query (generic path), C and V in sentinel form
+// (no size fields), needed-row ids and distances.
+void fill_bf_fast_layout(BfArgs& a) {
+    Carve c;
+    a.off_query = c.take(a.ld * 4);
+    a.off_cid = c.take(a.m * kSegPitch * 4);
+    a.off_cdist = c.take(a.m * kSegPitch * 4);
+    a.off_vid = c.take(a.m * kSegPitch * 4);
+    a.off_lst = c.take(64 * 4);
+    a.off_dl = c.take(64 * 4);
+    a.warp_smem = round_up(c.total, 16);
+}
+
 template <class K>
 int grid_for(K kernel, int threads, size_t smem, int sm_count, uint32_t work_warps,
              int warps_per_cta) {
@@ -396,6 +410,28 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
     a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
     a.batch_min = (uint32_t)std::max(0, env_int("TSDG_BATCH_MIN", 0));
+    // fast mode, k <= 31: register-direct warp-cooperative kernel (bf_fast.cuh);
+    // TSDG_FAST_KERNEL=staged keeps the staged kernel for comparison
+    if (mode == TSDG_MODE_FAST && a.k <= 31 && !env_is("TSDG_FAST_KERNEL", "staged")) {
+        // bit 0: bulk L2 prefetch of the rows past a hop's first batch (default, C2:
+        // 0.85 -> 0.79 ms); bit 1: L2 prefetch of admitted nodes' adjacency (slower)
+        a.prefetch = (uint32_t)env_int("TSDG_FAST_PREFETCH", 1);
+        fill_bf_fast_layout(a);
+        // row class: 1 = 128 floats, 2 = fewer (query in registers), 0 = generic
+        const bool reg_q = idx->ld <= 128 && idx->ld == idx->d &&
+                           (reinterpret_cast<uintptr_t>(d_queries) & 15u) == 0;
+        const int seg = reg_q ? (idx->ld == 128 ? 1 : 2) : 0;
+        const BfKernel kern =
+            bf_fast_kernel_for(idx->metric, seg, env_int("TSDG_FAST_VARIANT", 0));
+        const size_t smem = (size_t)a.warp_smem * kFastWarps;
+        set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast)");
+        const int grid = grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, kFastWarps);
+        kern<<<grid, kFastWarps * 32, smem, st>>>(a);
+        commit_counter(idx, tk, nq, (uint64_t)grid * kFastWarps);
+        g_launches++;
+        cuda_check(cudaGetLastError(), "bf_fast_kernel launch");
+        return;
+    }
     fill_bf_layout(a);
     const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
     const size_t smem = (size_t)a.warp_smem * wpc;
