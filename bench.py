@@ -223,7 +223,7 @@ def sharded_section(args, ws, rank, local, dev, dist):
         path = os.path.join(d, f"shard_{s}.tsdg")
         off, n = table[s]
         if not os.path.exists(path):
-            graph_pack.unpack(os.path.join(d, f"shard_{s}.pack.npz"), base[off:off + n], path)
+            graph_pack.unpack(os.path.join(d, f"shard_{s}.pk"), base[off:off + n], path)
         graphs[s] = load_tsdg(path)
         bases[s] = base[off:off + n]
     searcher = shards.ShardedSearcher(graphs, bases, table, device=local,
@@ -310,19 +310,62 @@ def dist_env():
     return ws, rank, local
 
 
-def reference_arm(args, ds, ws, rank):
-    """The reference's own CPU implementation (oracle/_ref) on the same config."""
+PREPARE = os.path.join(ROOT, "paper_2204_00824_b200", "_lib", "tsdg_prepare")
+
+
+def reference_inputs(name: str):
+    """Input files of `name` in the reference's formats, made (untimed) by the
+    tools/prepare_inputs.c executable when missing: base.fvecs / queries.fvecs
+    (checksum-verified seeded vectors) and graph.tsdg (rebuilt byte-identically from
+    graph.pk).  Returns (graph.tsdg, base.fvecs, queries.fvecs, gt).  Loads nothing
+    of this repository into the calling process."""
+    d = os.path.join(ROOT, "data", name)
+    with open(os.path.join(d, "meta.json")) as f:
+        meta = json.load(f)
+    sp = meta["spec"]
+    bpath, qpath, gpath = (os.path.join(d, x) for x in ("base.fvecs", "queries.fvecs", "graph.tsdg"))
+    if not (os.path.exists(bpath) and os.path.exists(qpath)):
+        subprocess.run([PREPARE, "vectors", sp["kind"], str(sp["n"]), str(sp["nq"]), str(sp["d"]),
+                        str(sp.get("latent", 0)), str(sp["clusters"]), repr(float(sp["spread"])),
+                        str(sp["seed"]), repr(float(sp.get("noise", 0.0))), bpath, qpath,
+                        meta["checksums"]["base"], meta["checksums"]["queries"]], check=True)
+    if not os.path.exists(gpath):
+        subprocess.run([PREPARE, "unpack", os.path.join(d, "graph.pk"), bpath, gpath], check=True)
+    gt = np.fromfile(os.path.join(d, "gt.u32"), np.uint32).reshape(sp["nq"], meta["gt_k"])
+    return gpath, bpath, qpath, gt
+
+
+def bench_config(ws: int, scaling: str) -> dict:
+    """The `config` object, identical on both arms."""
+    per_gpu = 10000 if scaling == "weak" else -(-10000 // ws)
+    return {"workload": WORKLOAD, "params": PARAMS, "scaling": scaling,
+            "queries_per_gpu": per_gpu, "global_batch": 10000 * ws if scaling == "weak" else 10000,
+            "parallelism": f"replicated index, {'each rank its own 10K batch' if scaling == 'weak' else 'the 10K batch split'} x{ws}"}
+
+
+def reference_arm(args, ws, rank):
+    """The reference's own CPU implementation, unmodified (oracle/_ref, compiled from
+    /root/reference): graph and vectors read by its load_tsdg / load_vectors, search
+    by its large_batch_search on all host threads; nothing of this repository's
+    search (or any library of it) is loaded into this process."""
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2204_00824_b200.search import BestFirstParams
 
+    gpath, bpath, qpath, gt = reference_inputs(DATASET)
     ref = O.Ref()
     threads = ref.so.ref_num_threads()
-    fx = ref.fixture(ds.graph_path, ds.base)
-    p = BestFirstParams(**PARAMS)
-    nq_step = min(args.ref_queries, ds.queries.shape[0])
-    q = ds.queries[:nq_step]
+    fx = ref.fixture_from_files(gpath, bpath)
+    queries = ref.load_vectors(qpath)
+
+    class P:  # BestFirstParams fields as the shim reads them
+        pass
+    p = P()
+    for kk, vv in PARAMS.items():
+        setattr(p, kk, vv)
+    p.unbounded = False
+    nq_step = min(args.ref_queries, queries.shape[0])
+    q = queries[:nq_step]
     for _ in range(args.warmup):
         fx.large_batch(q, p)
     t0 = time.perf_counter()
@@ -330,21 +373,44 @@ def reference_arm(args, ds, ws, rank):
         ids, counts, st = fx.large_batch(q, p)
     dt = time.perf_counter() - t0
     qps = nq_step * args.steps / dt
-    rec = O.recall_at_k(ids, counts, ds.gt, 10)
+    rec = recall_at_k(ids, counts, gt[:nq_step], 10)
+    rec1 = recall_at_k(ids, counts, gt[:nq_step], 1)
+    one = ref_one_thread(ref, fx, queries, p)
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (low-LID clustered, seeded)",
-        "config": {"workload": WORKLOAD, "params": PARAMS, "queries_per_step": nq_step,
-                   "recall_at_10": rec},
+        "config": bench_config(ws, args.scaling),
+        "recall_at_10": rec, "recall_at_1": rec1,
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
                          "sample": f"{nq_step} of the 10K C2 queries per step, reference "
-                                   f"large_batch_search (OpenMP, {threads} threads)"},
+                                   f"large_batch_search (OpenMP, {threads} threads); inputs read "
+                                   "by the reference's load_tsdg / load_vectors"},
+        "cpu_baseline_1thread": one,
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ref_one_thread(ref, fx, queries, p, seconds_budget=8.0):
+    """bench.cpp:321-345 also times the search on one thread: a bounded sample."""
+    full = ref.so.ref_num_threads()
+    ref.so.ref_set_num_threads(1)
+    try:
+        fx.large_batch(queries[:50], p)
+        t0 = time.perf_counter()
+        done = 0
+        while time.perf_counter() - t0 < seconds_budget and done < queries.shape[0]:
+            chunk = queries[done:done + 250]
+            fx.large_batch(chunk, p)
+            done += chunk.shape[0]
+        dt = time.perf_counter() - t0
+    finally:
+        ref.so.ref_set_num_threads(full)
+    return {"value": done / dt, "unit": "queries/s", "cores": 1, "kind": "reference",
+            "sample": f"first {done} C2 queries on 1 thread (~{seconds_budget:.0f}s)"}
 
 
 def cpu_baseline(ds, seconds_budget=15.0):
@@ -367,7 +433,8 @@ def cpu_baseline(ds, seconds_budget=15.0):
     dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "queries/s", "cores": threads, "kind": "reference",
             "sample": f"first {done} C2 queries, reference large_batch_search "
-                      f"(oracle/_ref, unmodified, OpenMP {threads} threads), ~{seconds_budget:.0f}s"}
+                      f"(oracle/_ref, unmodified, OpenMP {threads} threads), ~{seconds_budget:.0f}s",
+            "one_thread": ref_one_thread(ref, fx, ds.queries, p)}
 
 
 def main():
@@ -379,10 +446,17 @@ def main():
     ap.add_argument("--ref-queries", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["det", "fast"], default="fast")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: every rank searches its own 10K batch; strong: the 10K batch "
+                         "is split across the ranks (query_index_base = slice start)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the small-batch / sharded / C4 secondary measurements")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+
+    if args.impl == "reference":
+        reference_arm(args, ws, rank)
+        return
 
     from paper_2204_00824_b200 import datasets
 
@@ -392,9 +466,7 @@ def main():
         # builder (oracle/_ref, as for every benchmark graph), ground truth on the GPU
         cmd = [sys.executable, os.path.join(ROOT, "tools", "make_dataset.py"), "--name", DATASET,
                "--kind", "lowlid", "--n", "1000000", "--nq", "10000", "--d", "128", "--latent", "16",
-               "--builder", "nndescent", "--knn-k", "64", "--iters", "5"]
-        if args.impl != "reference":
-            cmd += ["--gt", "gpu"]
+               "--builder", "nndescent", "--knn-k", "64", "--iters", "5", "--gt", "gpu"]
         if ws > 1:  # one builder; the other ranks wait for its meta.json
             if rank == 0:
                 subprocess.run(cmd, check=True, stdout=sys.stderr)
@@ -407,10 +479,6 @@ def main():
             raise SystemExit(f"data/{DATASET} missing and oracle/_ref is not built: "
                              "bash tools/prepare_data.sh c2")
     ds = datasets.load(DATASET)
-
-    if args.impl == "reference":
-        reference_arm(args, ds, ws, rank)
-        return
 
     import torch
     import torch.distributed as dist
@@ -425,12 +493,20 @@ def main():
     graph = load_tsdg(ds.graph_path)
     idx = GpuIndex(graph, ds.base, device=local)
     p = BestFirstParams(**PARAMS)
-    nq, k = ds.queries.shape[0], p.k
-    qbase = rank * nq
+    k = p.k
+    if args.scaling == "strong":  # this rank's contiguous slice of the one 10K batch
+        per = -(-ds.queries.shape[0] // ws)
+        lo, hi = min(rank * per, ds.queries.shape[0]), min((rank + 1) * per, ds.queries.shape[0])
+        queries, gt, qbase = ds.queries[lo:hi], ds.gt[lo:hi], lo
+        total_q = ds.queries.shape[0]
+    else:  # every rank its own 10K batch, RNG streams continued (query_index_base)
+        queries, gt, qbase = ds.queries, ds.gt, rank * ds.queries.shape[0]
+        total_q = ds.queries.shape[0] * ws
+    nq = queries.shape[0]
 
     stream = torch.cuda.Stream(device=dev)
     sptr = stream.cuda_stream
-    dq = torch.from_numpy(ds.queries).to(dev)
+    dq = torch.from_numpy(queries).to(dev)
     d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
     d_counts = torch.empty(nq, dtype=torch.int32, device=dev)
@@ -469,7 +545,8 @@ def main():
         ids = d_ids.cpu().numpy().view(np.uint32).copy()
         counts = d_counts.cpu().numpy().view(np.uint32)
         stats = d_stats.cpu().numpy().astype(np.uint64)
-        rec = recall_at_k(ids, counts, ds.gt, 10)
+        rec = recall_at_k(ids, counts, gt, 10)
+        rec1 = recall_at_k(ids, counts, gt, 1)
         evals, examined = int(stats[:, 1].sum()), int(stats[:, 3].sum())
         alg_bytes = int(4 * d * evals + 4 * examined + nq * (4 * d + 8 * k))
         launches0 = _native.lib().tsdg_gpu_launch_count()
@@ -488,7 +565,8 @@ def main():
         ctx.__exit__(None, None, None)
         launches = _native.lib().tsdg_gpu_launch_count() - launches0
         total_s = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / 1e3)
-        return {"total_s": total_s, "value": nq * ws * args.steps / total_s, "recall_at_10": rec,
+        return {"total_s": total_s, "value": total_q * args.steps / total_s, "recall_at_10": rec,
+                "recall_at_1": rec1,
                 "alg_bytes": alg_bytes, "evals": evals, "examined": examined, "ids": ids,
                 "launches": int(launches)}
 
@@ -501,7 +579,7 @@ def main():
     kernel_s = head["total_s"] / args.steps  # one search kernel per step (+ a 4-byte memset)
 
     # ---- end-to-end through the host-pointer C-ABI call -----------------------------
-    hq = torch.from_numpy(ds.queries).pin_memory()
+    hq = torch.from_numpy(queries).pin_memory()
     h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
     h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
     h_c = torch.empty(nq, dtype=torch.int32).pin_memory()
@@ -526,7 +604,7 @@ def main():
         e2e_step()  # synchronous: returns after the D2H copies landed
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(e2e_times))
-    e2e_val = nq * ws * args.steps / e2e_s
+    e2e_val = total_q * args.steps / e2e_s
     assert np.array_equal(h_ids.numpy().view(np.uint32), head["ids"]), "e2e result differs"
 
     # ---- secondary workloads (not the headline): small batch, sharded base, C4 -----
@@ -557,21 +635,25 @@ def main():
             "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": head["total_s"] / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (low-LID clustered generator, seeded); graph built by the reference CPU builder",
-            "config": {"workload": WORKLOAD, "params": PARAMS, "mode": args.mode,
-                       "queries_per_gpu": nq, "global_batch": nq * ws,
-                       "parallelism": f"replicated index, query split x{ws}",
-                       "recall_at_10": head["recall_at_10"],
-                       "recall_at_10_reference": det["recall_at_10"],
-                       "l2": "flushed between timed steps (256 MB write); "
-                             "inputs also exceed L2 (512 MB vectors + padded adjacency)"},
+            "config": bench_config(ws, args.scaling),
+            "mode": args.mode,
+            "recall_at_10": head["recall_at_10"], "recall_at_1": head["recall_at_1"],
+            "recall_reference_order": {"recall_at_10": det["recall_at_10"],
+                                       "recall_at_1": det["recall_at_1"],
+                                       "note": "deterministic mode = the reference's results bit for bit"},
+            "l2": "flushed between timed steps (256 MB write); inputs also exceed L2 "
+                  "(512 MB vectors + padded adjacency)",
             "modes": {
                 "det": {"value": det["value"], "recall_at_10": det["recall_at_10"],
+                        "recall_at_1": det["recall_at_1"],
                         "note": "bit-exact with the reference (ids, distances, counters)"},
                 "fast": {"value": (head if head is not det else other)["value"],
                          "recall_at_10": (head if head is not det else other)["recall_at_10"],
-                         "note": "FMA distances; recall must stay within 0.5 pt of det"},
+                         "recall_at_1": (head if head is not det else other)["recall_at_1"],
+                         "note": "register-direct warp-cooperative gathers, FMA distances; "
+                                 "recall@1/@10 must stay within 0.5 pt of det"},
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -580,7 +662,7 @@ def main():
                          "evals_per_query": head["evals"] / nq,
                          "edges_per_query": head["examined"] / nq},
             "e2e": {"value": e2e_val, "unit": "queries/s",
-                    "h2d_bytes_per_step": int(ds.queries.nbytes),
+                    "h2d_bytes_per_step": int(queries.nbytes),
                     "d2h_bytes_per_step": int(nq * k * 8 + nq * 4),
                     "transfer": "zero-copy (kernel reads/writes pinned host memory)"
                     if os.environ.get("TSDG_ZERO_COPY", "1") != "0" else "copy pipeline (2 chunks, 2 streams)"},

@@ -369,6 +369,18 @@ class Ref:
             raise RuntimeError(self.err())
         return RefFixture(self, h, b.shape[1])
 
+    def fixture_from_files(self, tsdg_path, vectors_path):
+        """Graph and base loaded by the reference's own load_tsdg / load_vectors."""
+        so = self.so
+        so.ref_fixture_load_files.restype = ctypes.c_void_p
+        so.ref_fixture_load_files.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+        so.ref_fixture_d.restype = ctypes.c_uint32
+        so.ref_fixture_d.argtypes = [ctypes.c_void_p]
+        h = so.ref_fixture_load_files(tsdg_path.encode(), vectors_path.encode())
+        if not h:
+            raise RuntimeError(self.err())
+        return RefFixture(self, h, so.ref_fixture_d(ctypes.c_void_p(h)))
+
     def make_synthetic_split(self, n, nq, d, clusters, spread, seed):
         b = np.empty((n, d), np.float32)
         q = np.empty((nq, d), np.float32)

@@ -286,6 +286,23 @@ void* ref_fixture_load(const char* tsdg_path, const float* base, std::uint32_t n
     return fx;
 }
 
+// Both inputs through the reference's own loaders: load_tsdg (diversify.cpp:274-306)
+// and load_vectors (io.cpp:112-117) — bench.py's reference arm.
+void* ref_fixture_load_files(const char* tsdg_path, const char* vectors_path) {
+    auto* fx = new Fixture;
+    const int rc = guarded([&] {
+        fx->graph = load_tsdg(tsdg_path);
+        fx->base = load_vectors(vectors_path);
+    });
+    if (rc != 0) {
+        delete fx;
+        return nullptr;
+    }
+    return fx;
+}
+
+std::uint32_t ref_fixture_d(void* h) { return static_cast<Fixture*>(h)->base.d; }
+
 void ref_fixture_free(void* h) { delete static_cast<Fixture*>(h); }
 
 std::uint32_t ref_fixture_n(void* h) { return static_cast<Fixture*>(h)->graph.n; }

@@ -78,6 +78,19 @@ def build_datagen(force: bool = False) -> str:
     return out
 
 
+def build_prepare(force: bool = False) -> str:
+    """tools/prepare_inputs.c + datagen.c -> _lib/tsdg_prepare (an executable: the
+    reference arm of bench.py prepares its input files without loading a library of
+    this repository into its process)."""
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "tsdg_prepare")
+    srcs = [os.path.join(ROOT, "tools", f) for f in ("prepare_inputs.c", "datagen.c")]
+    if force or _stale(out, srcs):
+        _run(["gcc", "-std=c11", "-D_DEFAULT_SOURCE", "-O2", "-fopenmp", "-ffp-contract=off",
+              "-o", out, *srcs, "-lm"])
+    return out
+
+
 def build_oracle() -> None:
     _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"])
     if os.path.isdir("/root/reference/proj/src"):
@@ -92,6 +105,7 @@ def build_cpp_tests() -> None:
 
 def build_all(force: bool = False) -> None:
     build_datagen(force)
+    build_prepare(force)
     build_oracle()
     build_gpu(force)
     build_gpu_phases(force)

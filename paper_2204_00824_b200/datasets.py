@@ -104,7 +104,7 @@ class Dataset:
 
 def available(name: str) -> bool:
     d = os.path.join(DATA_DIR, name)
-    have_graph = any(os.path.exists(os.path.join(d, f)) for f in ("graph.tsdg", "graph.pack.npz"))
+    have_graph = any(os.path.exists(os.path.join(d, f)) for f in ("graph.tsdg", "graph.pk"))
     return have_graph and all(os.path.exists(os.path.join(d, f)) for f in ("meta.json", "gt.u32"))
 
 
@@ -125,6 +125,6 @@ def load(name: str, verify: bool = True) -> Dataset:
         sys.path.insert(0, ROOT)
         from tools import graph_pack
 
-        graph_pack.unpack(os.path.join(d, "graph.pack.npz"), base, gpath)
+        graph_pack.unpack(os.path.join(d, "graph.pk"), base, gpath)
     gt = np.fromfile(os.path.join(d, "gt.u32"), np.uint32).reshape(meta["spec"]["nq"], meta["gt_k"])
     return Dataset(name, base, queries, gpath, gt, meta)

@@ -1,13 +1,15 @@
 """Transport encoding of a reference-built TSDG file (saves push bandwidth to the
 GPU box; the search never reads this form).
 
-pack:   graph.tsdg -> graph.pack.npz  (header fields, degrees, and per edge the
+pack:   graph.tsdg -> graph.pk  (header fields, degrees, and per edge the
         target and lambda packed into ceil((bits(n)+bits(lambda0))/8) bytes; the
         fp32 edge distances are dropped because they are exactly recomputable)
-unpack: graph.pack.npz + base vectors -> graph.tsdg, byte-identical to the
+unpack: graph.pk + base vectors -> graph.tsdg, byte-identical to the
         original: distances recomputed in the reference's sequential fp32 order
         (tools/datagen.c tsdg_edge_distances), then the whole file's FNV-1a is
         checked against the checksum of the original recorded at pack time.
+        tools/prepare_inputs.c does the same from a base.fvecs file (the
+        reference arm of bench.py, which maps no library of this repository).
 """
 from __future__ import annotations
 
@@ -52,20 +54,45 @@ def _parse(path: str):
     return hdr, n, degs, targets, lambdas, dists
 
 
+PK_MAGIC = b"TSDGPK01"
+
+
 def pack(tsdg_path: str, out_path: str) -> None:
+    """graph.pk: "TSDGPK01" | u64 n | u64 E | u32 lbits | u32 nbytes | u64 fnv of the
+    original file | 27-byte header | n x u32 degrees | E x nbytes (target<<lbits|lambda).
+    Read by unpack() below and by the C tool tools/prepare_inputs.c."""
     hdr, n, degs, targets, lambdas, _ = _parse(tsdg_path)
     tbits = max(1, int(n - 1).bit_length())
     lbits = max(1, int(lambdas.max()).bit_length()) if lambdas.size else 1
     nbytes = (tbits + lbits + 7) // 8
     v = targets.astype(np.uint64) << np.uint64(lbits) | lambdas.astype(np.uint64)
     packed = v.view(np.uint8).reshape(-1, 8)[:, :nbytes].copy()
-    np.savez(out_path, header=hdr, degrees=degs, packed=packed,
-             lbits=np.array([lbits]), fnv=np.array([_fnv_file(tsdg_path)]))
+    fnv = int(_fnv_file(tsdg_path), 16)
+    with open(out_path, "wb") as f:
+        f.write(PK_MAGIC)
+        f.write(np.array([n, packed.shape[0]], "<u8").tobytes())
+        f.write(np.array([lbits, nbytes], "<u4").tobytes())
+        f.write(np.array([fnv], "<u8").tobytes())
+        f.write(hdr.tobytes())
+        f.write(degs.astype("<u4").tobytes())
+        f.write(packed.tobytes())
+
+
+def _read_pk(pack_path: str):
+    raw = np.fromfile(pack_path, np.uint8)
+    if raw[:8].tobytes() != PK_MAGIC:
+        raise RuntimeError(f"{pack_path}: not a graph pack")
+    n, E = (int(x) for x in raw[8:24].view("<u8"))
+    lbits, nbytes = (int(x) for x in raw[24:32].view("<u4"))
+    fnv = int(raw[32:40].view("<u8")[0])
+    hdr = raw[40:67].copy()
+    degs = raw[67:67 + 4 * n].view("<u4").copy()
+    packed = raw[67 + 4 * n:67 + 4 * n + E * nbytes].reshape(E, nbytes)
+    return hdr, degs, packed, lbits, fnv
 
 
 def unpack(pack_path: str, base: np.ndarray, out_path: str) -> None:
-    z = np.load(pack_path)
-    hdr, degs, packed, lbits = z["header"], z["degrees"], z["packed"], int(z["lbits"][0])
+    hdr, degs, packed, lbits, fnv = _read_pk(pack_path)
     n = degs.shape[0]
     metric = int(hdr[16])
     E = packed.shape[0]
@@ -97,16 +124,15 @@ def unpack(pack_path: str, base: np.ndarray, out_path: str) -> None:
     body[edge_pos[:, None] + np.arange(10)[None, :]] = rec
     tmp = f"{out_path}.tmp{os.getpid()}"  # unique per process: ranks may unpack concurrently
     body.tofile(tmp)
-    got = _fnv_file(tmp)
-    want = str(z["fnv"][0])
-    if got != want:
+    got = int(_fnv_file(tmp), 16)
+    if got != fnv:
         os.remove(tmp)
-        raise RuntimeError(f"unpacked TSDG differs from the original (fnv {got} != {want})")
+        raise RuntimeError(f"unpacked TSDG differs from the original (fnv {got:016x} != {fnv:016x})")
     os.replace(tmp, out_path)
 
 
 if __name__ == "__main__":
     name = sys.argv[1]
     d = os.path.join(datasets.DATA_DIR, name)
-    pack(os.path.join(d, "graph.tsdg"), os.path.join(d, "graph.pack.npz"))
-    print("packed", os.path.getsize(os.path.join(d, "graph.pack.npz")) / 1e6, "MB")
+    pack(os.path.join(d, "graph.tsdg"), os.path.join(d, "graph.pk"))
+    print("packed", os.path.getsize(os.path.join(d, "graph.pk")) / 1e6, "MB")

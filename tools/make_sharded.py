@@ -4,7 +4,7 @@ CPU builder (nn_descent + build(alpha, lambda0), knn_graph.cpp:141-251,
 diversify.cpp:152-209) over LOCAL ids; global id = shard offset + local id.
 
 data/<name>/meta.json        spec + shard table + checksums
-data/<name>/shard_<s>.tsdg   per-shard TSDG (plus shard_<s>.pack.npz transport form)
+data/<name>/shard_<s>.tsdg   per-shard TSDG (plus shard_<s>.pk transport form)
 data/<name>/gt.u32           exact top-gt_k over the WHOLE base (reference ground_truth)
 
 python tools/make_sharded.py --name c5s_lowlid_2m_96 --n 2000000 --nq 10000 --d 96 \
@@ -70,7 +70,7 @@ def main():
                                 ctypes.c_uint32(0), path.encode(), stats)
         if rc:
             raise RuntimeError(ref.ref_last_error().decode())
-        graph_pack.pack(path, os.path.join(out, f"shard_{s}.pack.npz"))
+        graph_pack.pack(path, os.path.join(out, f"shard_{s}.pk"))
         shards.append({"offset": lo, "n": hi - lo, "build_stats": list(stats),
                        "build_seconds": round(time.time() - t0, 1)})
         print(f"[make_sharded] shard {s}: {hi-lo} nodes in {time.time()-t0:.1f}s", flush=True)
