@@ -223,7 +223,8 @@ def sharded_section(args, ws, rank, local, dev, dist):
         path = os.path.join(d, f"shard_{s}.tsdg")
         off, n = table[s]
         if not os.path.exists(path):
-            graph_pack.unpack(os.path.join(d, f"shard_{s}.pk"), base[off:off + n], path)
+            bpath, _ = datasets.ensure_fvecs(SHARDED, base, queries)
+            graph_pack.unpack(os.path.join(d, f"shard_{s}.pk"), bpath, path, off)
         graphs[s] = load_tsdg(path)
         bases[s] = base[off:off + n]
     searcher = shards.ShardedSearcher(graphs, bases, table, device=local,

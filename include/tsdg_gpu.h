@@ -173,6 +173,22 @@ int tsdg_gpu_greedy_once(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
                          const uint64_t* rng_states, uint32_t hop_limit, uint32_t lambda_cut,
                          uint32_t* ids32, float* dists32, tsdg_query_stats* stats);
 
+/* ---- persistent small-batch server (small_batch_search, greedy_search.cpp:106-127)
+ * The latency form of tsdg_gpu_search_greedy: the cluster-per-query kernel stays
+ * resident on the GPU and is fed through mapped pinned host memory, so a request
+ * costs no kernel launch, copy or stream synchronisation (the calling thread spins
+ * on the response word).  Same results as tsdg_gpu_search_greedy with the same
+ * (k, params, mode).  Limits: t0 <= 16, k <= 64, nq <= max_batch per request; the
+ * server occupies min(max_batch, co-resident clusters) x t0 CTAs until destroyed.
+ * Requests on one server are serialised (internal mutex). */
+typedef struct tsdg_gpu_server tsdg_gpu_server;
+int tsdg_gpu_server_create(tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* params,
+                           int mode, uint32_t max_batch, tsdg_gpu_server** out);
+int tsdg_gpu_server_search(tsdg_gpu_server* server, const float* queries, uint32_t nq,
+                           uint32_t* ids, float* dists, uint32_t* counts);
+int tsdg_gpu_server_info(const tsdg_gpu_server* server, uint32_t* clusters, uint32_t* max_batch);
+int tsdg_gpu_server_destroy(tsdg_gpu_server* server);
+
 /* ---- sharded base: per-shard top-k merge (no reference counterpart) ----------
  * After an all-gather of S shards' results (each nq x k, LOCAL ids, ascending),
  * merges per query by (dist, global id), global id = shard_base[s] + local id.

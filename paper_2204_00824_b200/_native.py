@@ -62,6 +62,10 @@ SIGNATURES = {
     "tsdg_gpu_search_greedy_device": (_I, [_VP, _VP, _U32, _U32, _VP, _I, _VP, _VP, _VP, _VP,
                                            _VP]),
     "tsdg_gpu_greedy_once": (_I, [_VP, _VP, _U32, _VP, _U32, _U32, _VP, _VP, _VP]),
+    "tsdg_gpu_server_create": (_I, [_VP, _U32, _VP, _I, _U32, _VP]),
+    "tsdg_gpu_server_search": (_I, [_VP, _VP, _U32, _VP, _VP, _VP]),
+    "tsdg_gpu_server_info": (_I, [_VP, _VP, _VP]),
+    "tsdg_gpu_server_destroy": (_I, [_VP]),
     "tsdg_gpu_merge_shards_device": (_I, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _VP, _VP, _VP,
                                           _VP]),
     "tsdg_gpu_ground_truth": (_I, [_VP, _U32, _VP, _U32, _U32, _U32, _I, _I, _VP, _VP]),

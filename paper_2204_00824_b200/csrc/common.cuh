@@ -21,6 +21,19 @@ namespace tsdg_dev {
 #ifdef TSDG_PHASES
 __device__ unsigned long long g_phase[1 << 16][8];
 __device__ __forceinline__ unsigned gwarp_id() { return (blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
+// Per-CTA event trace (globaltimer ns) for the small-batch kernels: thread 0 of CTA b
+// writes slot i of g_trace[b] (tools/trace_small.py reads it).
+__device__ unsigned long long g_trace[256][32];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TR_MARK(i)                                                                      \
+    {                                                                                   \
+        if (threadIdx.x == 0 && blockIdx.x < 256 && (i) < 32)                           \
+            tsdg_dev::g_trace[blockIdx.x][(i)] = tsdg_dev::gtimer();                    \
+    }
 #define PH_DECL long long _ph = clock64();
 #define PH_RESET _ph = clock64();
 #define PH_MARK(i)                                                                      \
@@ -33,6 +46,7 @@ __device__ __forceinline__ unsigned gwarp_id() { return (blockIdx.x * blockDim.x
 #define PH_DECL
 #define PH_RESET
 #define PH_MARK(i)
+#define TR_MARK(i)
 #endif
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;

@@ -179,6 +179,44 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
 // One CTA per query: pool the t0 x 32 walk slots, sort, unique, first k.
 constexpr int kMergeThreads = 256;
 
+// k-way merge of up to 32 lists sorted by (dist, id) (list r = entries
+// [r*stride, r*stride + len); an invalid id ends a list) into the first k DISTINCT ids
+// in (dist, id) order — the reference's pool sort + unique + first k
+// (greedy_search.cpp:85-103) without sorting the pool: lane r holds list r's head and
+// each step takes the warp arg-min.  A repeated id carries the same distance, so every
+// list holding it has it at its head at that step and all of them advance together.
+// Warp-uniform call; out(i, id, dist) is invoked by every lane; returns the count.
+template <class Out>
+__device__ __forceinline__ uint32_t warp_kway_unique(const float* ld, const uint32_t* li,
+                                                     uint32_t nlists, uint32_t len,
+                                                     uint32_t stride, uint32_t k, int lane,
+                                                     Out out) {
+    const float kInf = __int_as_float(0x7f800000);
+    uint32_t pos = 0;
+    float hd = kInf;
+    uint32_t hi = kInvalid;
+    const bool mine = (uint32_t)lane < nlists;
+    if (mine && len > 0) {
+        hi = li[(size_t)lane * stride];
+        hd = hi != kInvalid ? ld[(size_t)lane * stride] : kInf;
+    }
+    uint32_t cnt = 0;
+    while (cnt < k) {
+        float bd = hd;
+        uint32_t bi = hi;
+        warp_argmin(bd, bi);
+        if (bi == kInvalid) break;
+        out(cnt, bi, bd);
+        ++cnt;
+        if (hi == bi) {
+            ++pos;
+            hi = pos < len ? li[(size_t)lane * stride + pos] : kInvalid;
+            hd = hi != kInvalid ? ld[(size_t)lane * stride + pos] : kInf;
+        }
+    }
+    return cnt;
+}
+
 __global__ void __launch_bounds__(kMergeThreads) greedy_merge_kernel(
     const uint32_t* walk_ids, const float* walk_dists, const uint32_t* walk_hops,
     const uint32_t* walk_evals, uint32_t t0, uint32_t k, uint32_t npow2, uint32_t* out_ids,

@@ -69,31 +69,70 @@ struct GcCtl {
     uint32_t u_next;  // next node, published before the merge (L2 warm-up)
 };
 
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// Output targets of one query (the launch path: the result arrays; the server:
+// mapped host memory).
+struct GcOut {
+    uint32_t* ids;  // k entries for this query
+    float* dists;   // or nullptr
+    uint32_t* count;
+    tsdg_query_stats* stats;  // or nullptr
+};
+
+// Shared-memory views of one CTA (carved by the host, GcArgs::off_*).
+struct GcSmem {
+    float* sq;
+    GcPart* part;
+    GcCtl* ctl;
+    float* list_d;
+    uint32_t* list_i;
+    float* pool_d;     // rank 0: the t0 walk lists, pushed by the walks over DSMEM
+    uint32_t* pool_i;
+    uint32_t* scan;
+    uint32_t* walk_cnt;  // rank 0: 2 x t0 (hops, evals) pushed by the walks
+};
+
+__device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_raw) {
+    GcSmem m;
+    m.sq = reinterpret_cast<float*>(smem_raw + a.off_query);
+    m.part = reinterpret_cast<GcPart*>(smem_raw + a.off_part);
+    m.ctl = reinterpret_cast<GcCtl*>(smem_raw + a.off_ctl);
+    m.list_d = reinterpret_cast<float*>(smem_raw + a.off_list);
+    m.list_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_list + 32 * 4);
+    m.pool_d = reinterpret_cast<float*>(smem_raw + a.off_pool);
+    m.pool_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_pool + a.npow2 * 4);
+    m.scan = m.pool_i + a.npow2;
+    m.walk_cnt = m.scan + kGcThreads + 1;
+    return m;
+}
+
+// One walk (CTA) of query q: select_start + hops + (cluster mode) the in-cluster merge
+// of the t0 walks into `o`.  gq: the query (any memory space the SM can read: device
+// memory, or mapped host memory for the server); s: the walk's RNG stream index.
 template <int METRIC, bool FAST, int STAGE>
-__global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+__device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpStage& w,
+                                         uint32_t s, uint32_t walk, const float* gq,
+                                         const GcOut& o) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t walk = blockIdx.x;
-    const uint32_t q = walk / a.t0, s = walk % a.t0;
-    float* sq = reinterpret_cast<float*>(smem_raw + a.off_query);
-    GcPart* part = reinterpret_cast<GcPart*>(smem_raw + a.off_part);
-    GcCtl* ctl = reinterpret_cast<GcCtl*>(smem_raw + a.off_ctl);
-    float* list_d = reinterpret_cast<float*>(smem_raw + a.off_list);
-    uint32_t* list_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_list + 32 * 4);
-    const uint32_t pitch = a.dch + 4;
-    WarpStage w;
-    w.sq = sq;
-    w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * pitch;
-    w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
-    w.parity = 0;
-    w.rowid = STAGE == kStageLdgsts ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;
+    float* sq = m.sq;
+    GcPart* part = m.part;
+    GcCtl* ctl = m.ctl;
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     const float kInf = __int_as_float(0x7f800000);
 
-    const float* gq = a.queries + (size_t)q * a.d;
+    TR_MARK(0)
+    // the walks push into rank 0's shared memory when they end: arrive now, wait
+    // before the push (every CTA of the cluster has started by then)
+    if (a.cluster) cluster_arrive_relaxed();
     for (uint32_t i = threadIdx.x; i < a.ld; i += blockDim.x) sq[i] = i < a.d ? gq[i] : 0.0f;
-    if (lane == 0) mbar_init(w.bar, 1);
     __syncthreads();
+    TR_MARK(1)
 
     // select_start (greedy_search.cpp:12-25) by warp 0
     if (warp == 0) {
@@ -128,6 +167,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
         e0 = pend ? __ldg(a.adj + (size_t)u * a.R + j0) : kInvalid;
         gather_issue(w, g, pend, e0, lane);
     }
+    TR_MARK(2)
     PH_DECL
     PH_MARK(0)  // phase 0: query load + select_start
     while (ctl->improved && t < a.hop_limit) {
@@ -221,6 +261,7 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
         }
         PH_MARK(3)  // warp 0: combine + merge_halves
         __syncthreads();
+        TR_MARK(3 + t)
         PH_MARK(4)  // barrier
     }
     if (pipe) gather_complete<METRIC, FAST>(w, g, pend, lane);  // drain a pre-issued group
@@ -238,109 +279,156 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
         return;
     }
 
-    // ---- in-cluster merge over DSMEM (CTA rank 0 of the query's cluster) ---------
-    if (warp == 0) {
-        list_d[lane] = rd;
-        list_i[lane] = ri;
-        if (lane == 0) ctl->hops = t;
-    }
+    // ---- in-cluster merge (CTA rank 0 of the query's cluster) ----------------------
+    // each walk pushes its sorted 32-slot list and counters into rank 0's shared
+    // memory over DSMEM as soon as it ends, so the merge reads local memory only
     cg::cluster_group cluster = cg::this_cluster();
+    cluster_wait();
+    if (warp == 0) {
+        float* rpd = cluster.map_shared_rank(m.pool_d, 0);
+        uint32_t* rpi = cluster.map_shared_rank(m.pool_i, 0);
+        rpd[s * 32 + lane] = ri != kInvalid ? rd : kInf;
+        rpi[s * 32 + lane] = ri;
+        if (lane == 0) {
+            uint32_t* rwc = cluster.map_shared_rank(m.walk_cnt, 0);
+            rwc[2 * s] = t;
+            rwc[2 * s + 1] = ctl->evals;
+        }
+    }
+    TR_MARK(27)
     cluster.sync();
+    TR_MARK(28)
     PH_MARK(6)  // waiting for the slowest walk of the query
     if (cluster.block_rank() == 0) {
-        float* pd = reinterpret_cast<float*>(smem_raw + a.off_pool);
-        uint32_t* pi = reinterpret_cast<uint32_t*>(smem_raw + a.off_pool + a.npow2 * 4);
-        uint32_t* scan = pi + a.npow2;  // blockDim + 1
-        const uint32_t total = a.t0 * 32;
-        for (uint32_t i = threadIdx.x; i < a.npow2; i += blockDim.x) {
-            float dd = kInf;
-            uint32_t id = kInvalid;
-            if (i < total) {
-                const uint32_t r = i / 32, slot = i % 32;
-                const float* rl = cluster.map_shared_rank(list_d, r);
-                const uint32_t* il = cluster.map_shared_rank(list_i, r);
-                id = il[slot];
-                dd = id != kInvalid ? rl[slot] : kInf;
-            }
-            pd[i] = dd;
-            pi[i] = id;
-        }
+        float* pd = m.pool_d;
+        uint32_t* pi = m.pool_i;
+        uint32_t* scan = m.scan;
         uint32_t hsum = 0, esum = 0;
-        if (threadIdx.x == 0) {
-            for (uint32_t r = 0; r < a.t0; ++r) {
-                const GcCtl* rc = cluster.map_shared_rank(ctl, r);
-                hsum += rc->hops;
-                esum += rc->evals;
+        if (warp == 0) {
+            for (uint32_t r = lane; r < a.t0; r += 32) {
+                hsum += m.walk_cnt[2 * r];
+                esum += m.walk_cnt[2 * r + 1];
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                hsum += __shfl_xor_sync(kFull, hsum, off);
+                esum += __shfl_xor_sync(kFull, esum, off);
             }
         }
-        __syncthreads();
-        for (uint32_t kk = 2; kk <= a.npow2; kk <<= 1) {
-            for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-                for (uint32_t i = threadIdx.x; i < a.npow2; i += blockDim.x) {
-                    const uint32_t p = i ^ j;
-                    if (p > i) {
-                        const bool up = (i & kk) == 0;
-                        const bool p_first = closer(pd[p], pi[p], pd[i], pi[i]);
-                        if (p_first == up) {
-                            const float td = pd[i];
-                            const uint32_t ti = pi[i];
-                            pd[i] = pd[p];
-                            pi[i] = pi[p];
-                            pd[p] = td;
-                            pi[p] = ti;
+        uint32_t c = 0;
+        if (a.k <= 64 && a.t0 <= 32) {
+            // the t0 lists are sorted: a warp k-way merge of their heads (k steps)
+            if (warp == 0) {
+                c = warp_kway_unique(pd, pi, a.t0, 32, 32, a.k, lane,
+                                     [&](uint32_t i, uint32_t id, float dd) {
+                                         if (lane == 0) {
+                                             o.ids[i] = id;
+                                             if (o.dists) o.dists[i] = dd;
+                                         }
+                                     });
+                for (uint32_t i = c + lane; i < a.k; i += 32) {
+                    o.ids[i] = kInvalid;
+                    if (o.dists) o.dists[i] = kInf;
+                }
+            }
+        } else {
+            for (uint32_t i = a.t0 * 32 + threadIdx.x; i < a.npow2; i += blockDim.x) {
+                pd[i] = kInf;
+                pi[i] = kInvalid;
+            }
+            __syncthreads();
+            for (uint32_t kk = 2; kk <= a.npow2; kk <<= 1) {
+                for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+                    for (uint32_t i = threadIdx.x; i < a.npow2; i += blockDim.x) {
+                        const uint32_t p = i ^ j;
+                        if (p > i) {
+                            const bool up = (i & kk) == 0;
+                            const bool p_first = closer(pd[p], pi[p], pd[i], pi[i]);
+                            if (p_first == up) {
+                                const float td = pd[i];
+                                const uint32_t ti = pi[i];
+                                pd[i] = pd[p];
+                                pi[i] = pi[p];
+                                pd[p] = td;
+                                pi[p] = ti;
+                            }
                         }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
-        }
-        const uint32_t per = (a.npow2 + blockDim.x - 1) / blockDim.x;
-        const uint32_t b0 = threadIdx.x * per;
-        uint32_t cnt = 0;
-        for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i)
-            cnt += (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) ? 1u : 0u;
-        scan[threadIdx.x] = cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (uint32_t x = 0; x < blockDim.x; ++x) {
-                const uint32_t c = scan[x];
-                scan[x] = run;
-                run += c;
-            }
-            scan[blockDim.x] = run;
-        }
-        __syncthreads();
-        uint32_t pos = scan[threadIdx.x];
-        for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i) {
-            if (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) {
-                if (pos < a.k) {
-                    a.out_ids[(size_t)q * a.k + pos] = pi[i];
-                    if (a.out_dists) a.out_dists[(size_t)q * a.k + pos] = pd[i];
+            const uint32_t per = (a.npow2 + blockDim.x - 1) / blockDim.x;
+            const uint32_t b0 = threadIdx.x * per;
+            uint32_t cnt = 0;
+            for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i)
+                cnt += (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) ? 1u : 0u;
+            scan[threadIdx.x] = cnt;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t run = 0;
+                for (uint32_t x = 0; x < blockDim.x; ++x) {
+                    const uint32_t cc = scan[x];
+                    scan[x] = run;
+                    run += cc;
                 }
-                ++pos;
+                scan[blockDim.x] = run;
+            }
+            __syncthreads();
+            uint32_t pos = scan[threadIdx.x];
+            for (uint32_t i = b0; i < b0 + per && i < a.npow2; ++i) {
+                if (pi[i] != kInvalid && (i == 0 || pi[i] != pi[i - 1])) {
+                    if (pos < a.k) {
+                        o.ids[pos] = pi[i];
+                        if (o.dists) o.dists[pos] = pd[i];
+                    }
+                    ++pos;
+                }
+            }
+            const uint32_t uniq = scan[blockDim.x];
+            c = uniq < a.k ? uniq : a.k;
+            for (uint32_t i = c + threadIdx.x; i < a.k; i += blockDim.x) {
+                o.ids[i] = kInvalid;
+                if (o.dists) o.dists[i] = kInf;
             }
         }
-        const uint32_t uniq = scan[blockDim.x];
-        const uint32_t c = uniq < a.k ? uniq : a.k;
-        for (uint32_t i = c + threadIdx.x; i < a.k; i += blockDim.x) {
-            a.out_ids[(size_t)q * a.k + i] = kInvalid;
-            if (a.out_dists) a.out_dists[(size_t)q * a.k + i] = kInf;
-        }
         if (threadIdx.x == 0) {
-            if (a.out_counts) a.out_counts[q] = c;
-            if (a.out_stats) {
+            if (o.count) *o.count = c;
+            if (o.stats) {
                 tsdg_query_stats st;
                 st.hops = hsum;
                 st.distance_evals = esum;
                 st.queue_evictions = 0;
                 st.edges_examined = esum - 32u * a.t0;
-                a.out_stats[q] = st;
+                *o.stats = st;
             }
         }
     }
     PH_MARK(7)  // rank 0: pool merge
-    cluster.sync();  // siblings stay resident until rank 0 has read their lists
+    TR_MARK(29)
+    cluster.sync();  // rank 0's pool is free again before the walks of a next query push
+    TR_MARK(30)
+}
+
+template <int METRIC, bool FAST, int STAGE>
+__global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t walk = blockIdx.x;
+    const uint32_t q = walk / a.t0, s = walk % a.t0;
+    const GcSmem m = gc_smem(a, smem_raw);
+    WarpStage w;
+    w.sq = m.sq;
+    w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * (a.dch + 4);
+    w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
+    w.parity = 0;
+    w.rowid = STAGE == kStageLdgsts ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;
+    if (lane == 0) mbar_init(w.bar, 1);
+    GcOut o;
+    o.ids = a.out_ids ? a.out_ids + (size_t)q * a.k : nullptr;
+    o.dists = a.out_dists ? a.out_dists + (size_t)q * a.k : nullptr;
+    o.count = a.out_counts ? a.out_counts + q : nullptr;
+    o.stats = a.out_stats ? a.out_stats + q : nullptr;
+    gc_query<METRIC, FAST, STAGE>(a, m, w, s, walk, a.queries + (size_t)q * a.d, o);
 }
 
 }  // namespace tsdg_dev

@@ -108,6 +108,29 @@ def available(name: str) -> bool:
     return have_graph and all(os.path.exists(os.path.join(d, f)) for f in ("meta.json", "gt.u32"))
 
 
+def write_fvecs(path: str, a: np.ndarray) -> None:
+    """fvecs (io.cpp:58-121 format: per row an int32 dimension, then the floats)."""
+    a = np.ascontiguousarray(a, np.float32)
+    rec = np.empty((a.shape[0], a.shape[1] + 1), np.float32)
+    rec[:, 0] = np.array([a.shape[1]], np.int32).view(np.float32)[0]
+    rec[:, 1:] = a
+    tmp = f"{path}.tmp{os.getpid()}"
+    rec.tofile(tmp)
+    os.replace(tmp, path)
+
+
+def ensure_fvecs(name: str, base: np.ndarray, queries: np.ndarray):
+    """data/<name>/base.fvecs and queries.fvecs (the files the reference's loaders and
+    tools/prepare_inputs.c read), written from the in-memory vectors when missing."""
+    d = os.path.join(DATA_DIR, name)
+    bpath, qpath = os.path.join(d, "base.fvecs"), os.path.join(d, "queries.fvecs")
+    if not os.path.exists(bpath):
+        write_fvecs(bpath, base)
+    if not os.path.exists(qpath):
+        write_fvecs(qpath, queries)
+    return bpath, qpath
+
+
 def load(name: str, verify: bool = True) -> Dataset:
     d = os.path.join(DATA_DIR, name)
     with open(os.path.join(d, "meta.json")) as f:
@@ -125,6 +148,7 @@ def load(name: str, verify: bool = True) -> Dataset:
         sys.path.insert(0, ROOT)
         from tools import graph_pack
 
-        graph_pack.unpack(os.path.join(d, "graph.pk"), base, gpath)
+        bpath, _ = ensure_fvecs(name, base, queries)
+        graph_pack.unpack(os.path.join(d, "graph.pk"), bpath, gpath)
     gt = np.fromfile(os.path.join(d, "gt.u32"), np.uint32).reshape(meta["spec"]["nq"], meta["gt_k"])
     return Dataset(name, base, queries, gpath, gt, meta)

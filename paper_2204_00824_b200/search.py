@@ -258,6 +258,11 @@ class GpuIndex:
                                            _p(ids), _p(dists), _p(counts), _p(stats)))
         return SearchResult(ids, dists, counts, stats)
 
+    def greedy_server(self, k: int, params: GreedyParams = GreedyParams(), *,
+                      mode: int = _native.MODE_DETERMINISTIC, max_batch: int = 64) -> "GreedyServer":
+        """Persistent small-batch server over this index (tsdg_gpu_server_*)."""
+        return GreedyServer(self, k, params, mode=mode, max_batch=max_batch)
+
     def small_batch_search(self, queries, k: int, params: GreedyParams = GreedyParams(),
                            stats: Optional[SearchStats] = None, **kw) -> List[np.ndarray]:
         r = self.search_greedy(queries, k, params, **kw)
@@ -559,3 +564,56 @@ __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "Ts
            "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
            "BuildStats", "build", "MultiGpuIndex", "ShardedGpuIndex",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]
+
+
+class GreedyServer:
+    """Resident small-batch (Alg. 1) search: the cluster-per-query kernel stays on the
+    GPU and takes requests through mapped pinned memory (tsdg_gpu_server_*), so a
+    call pays no launch or copy.  Results equal GpuIndex.search_greedy with the same
+    (k, params, mode).  Use as a context manager or call close()."""
+
+    def __init__(self, index: "GpuIndex", k: int, params: GreedyParams = GreedyParams(), *,
+                 mode: int = _native.MODE_DETERMINISTIC, max_batch: int = 64):
+        self.index, self.k, self.max_batch = index, int(k), int(max_batch)
+        self._keep = index  # the index must outlive the server
+        h = ctypes.c_void_p()
+        pc = params.c()
+        check(lib().tsdg_gpu_server_create(index._h, int(k), ctypes.byref(pc), int(mode),
+                                           self.max_batch, ctypes.byref(h)))
+        self._h = h
+        c, mb = ctypes.c_uint32(), ctypes.c_uint32()
+        check(lib().tsdg_gpu_server_info(h, ctypes.byref(c), ctypes.byref(mb)))
+        self.clusters = int(c.value)
+        self._ids = np.empty((self.max_batch, max(self.k, 1)), np.uint32)
+        self._dists = np.empty((self.max_batch, max(self.k, 1)), np.float32)
+        self._counts = np.empty(self.max_batch, np.uint32)
+
+    def search(self, queries) -> SearchResult:
+        q = _f32rows(queries, self.index.d)
+        nq = q.shape[0]
+        ids, dists, counts = self._ids[:nq], self._dists[:nq], self._counts[:nq]
+        check(lib().tsdg_gpu_server_search(self._h, _p(q), nq, _p(ids), _p(dists), _p(counts)))
+        return SearchResult(ids.copy(), dists.copy(), counts.copy(), np.zeros(nq, QUERY_STATS_DTYPE))
+
+    def search_into(self, q_ptr: int, nq: int, ids_ptr: int, dists_ptr: int, counts_ptr: int) -> None:
+        """Raw-pointer form (host buffers) for latency measurement."""
+        check(lib().tsdg_gpu_server_search(self._h, ctypes.c_void_p(q_ptr), nq,
+                                           ctypes.c_void_p(ids_ptr), ctypes.c_void_p(dists_ptr),
+                                           ctypes.c_void_p(counts_ptr)))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            check(lib().tsdg_gpu_server_destroy(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
