@@ -162,22 +162,41 @@ def _events_time(fn, steps, stream=None):
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def small_batch_section(idx, ds, dev):
-    """Alg. 1 (greedy, CTA/cluster kernel for small batches) latency on C2:
-    batch 1 / 8 / 64, t0 = 16 (recall@10 >= 0.95), queries resident on the device."""
+def small_batch_section(idx, ds, dev, ref_fx=None):
+    """C3: Alg. 1 (greedy, CTA/cluster-per-query procedure) on the C2 index at batch
+    1 / 8 / 64, at the cheapest t0 whose recall@10 reaches 0.95 (the reference's
+    small_batch_search gives the same ids: deterministic mode is bit-exact).
+      device:  launch path, queries resident in HBM, CUDA events around each call
+      e2e:     the persistent server (tsdg_gpu_server_search) with pinned HOST query /
+               result buffers, wall clock around each synchronous call
+      launch:  the host-pointer launch call (tsdg_gpu_search_greedy), wall clock
+      reference: the reference's small_batch_search (oracle/_ref, all host threads)
+               on the same queries, wall clock per call"""
     import torch
 
     from paper_2204_00824_b200.search import GreedyParams
 
-    out = []
-    p = GreedyParams(t0=16, hop_limit=16, lambda_cut=10, seed=7)
     k = 10
+    # cheapest t0 reaching recall@10 >= 0.95 on the first 2000 queries (untimed)
+    t0_pick, sweep = None, {}
+    for t0 in (8, 10, 12, 16):
+        p = GreedyParams(t0=t0, hop_limit=16, lambda_cut=10, seed=7)
+        r = idx.search_greedy(ds.queries[:2000], k, p)
+        sweep[t0] = recall_at_k(r.ids, r.counts, ds.gt[:2000], 10)
+        if sweep[t0] >= 0.95:
+            t0_pick = t0
+            break
+    t0_pick = t0_pick or 16
+    p = GreedyParams(t0=t0_pick, hop_limit=16, lambda_cut=10, seed=7)
+    out = []
     for batch in (1, 8, 64):
-        reps = 256 if batch == 1 else 1024 // batch
-        dq = torch.from_numpy(ds.queries[:reps * batch]).to(dev)
-        ids = torch.empty((reps * batch, k), dtype=torch.int32, device=dev)
-        dd = torch.empty((reps * batch, k), dtype=torch.float32, device=dev)
-        cc = torch.empty(reps * batch, dtype=torch.int32, device=dev)
+        reps = 256 if batch == 1 else max(32, 1024 // batch)
+        nq = reps * batch
+        row = {"batch": batch, "t0": p.t0}
+        dq = torch.from_numpy(ds.queries[:nq]).to(dev)
+        ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        dd = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        cc = torch.empty(nq, dtype=torch.int32, device=dev)
         st = torch.cuda.current_stream(dev).cuda_stream
 
         def call(j):
@@ -190,13 +209,81 @@ def small_batch_section(idx, ds, dev):
         times = []
         for j in range(reps):  # one call at a time: latency, not throughput
             times += _events_time(lambda: call(j), 1)
-        rec = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(),
-                          ds.gt[:reps * batch], 10)
+        row["recall_at_10"] = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(),
+                                          ds.gt[:nq], 10)
+        row["recall_at_1"] = recall_at_k(ids.cpu().numpy().view(np.uint32), cc.cpu().numpy(),
+                                         ds.gt[:nq], 1)
         lat = float(np.median(times))
-        out.append({"batch": batch, "t0": p.t0, "latency_ms_p50": lat,
-                    "latency_ms_p99": float(np.percentile(times, 99)),
-                    "qps": batch / lat * 1e3, "recall_at_10": rec})
-    return {"procedure": "greedy (paper Alg. 1), deterministic, C2 index", "points": out}
+        row["device"] = {"latency_us_p50": lat * 1e3, "latency_us_p99": float(np.percentile(times, 99)) * 1e3,
+                         "qps": batch / lat * 1e3}
+        dev_ids = ids.cpu().numpy().view(np.uint32).copy()
+        # end to end with host buffers: the resident server, then the launch call
+        hq = torch.from_numpy(ds.queries[:nq].copy()).pin_memory()
+        hi = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+        hd = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        hc = torch.empty(nq, dtype=torch.int32).pin_memory()
+        with idx.greedy_server(k, p, max_batch=batch) as sv:
+            def scall(j):
+                o = j * batch
+                sv.search_into(hq[o].data_ptr(), batch, hi[o].data_ptr(), hd[o].data_ptr(), hc[o].data_ptr())
+            for j in range(5):
+                scall(j)
+            lat_s = []
+            for j in range(reps):
+                t = time.perf_counter()
+                scall(j)
+                lat_s.append(time.perf_counter() - t)
+        assert np.array_equal(hi.numpy().view(np.uint32), dev_ids), "server result differs"
+        m = float(np.median(lat_s))
+        row["e2e"] = {"path": "persistent server (tsdg_gpu_server_search), pinned host buffers",
+                      "latency_us_p50": m * 1e6, "latency_us_p99": float(np.percentile(lat_s, 99)) * 1e6,
+                      "qps": batch / m, "h2d_bytes_per_call": batch * ds.queries.shape[1] * 4,
+                      "d2h_bytes_per_call": batch * (k * 8 + 4)}
+        L = _native_lib()
+        pc = p.c()
+
+        def lcall(j):
+            o = j * batch
+            _native_check(L.tsdg_gpu_search_greedy(
+                idx.handle, ctypes.c_void_p(hq[o].data_ptr()), batch, k, ctypes.byref(pc), 0,
+                ctypes.c_void_p(hi[o].data_ptr()), ctypes.c_void_p(hd[o].data_ptr()),
+                ctypes.c_void_p(hc[o].data_ptr()), None))
+
+        for j in range(3):
+            lcall(j)
+        lat_l = []
+        for j in range(min(reps, 128)):
+            t = time.perf_counter()
+            lcall(j)
+            lat_l.append(time.perf_counter() - t)
+        row["launch_host_call_us_p50"] = float(np.median(lat_l)) * 1e6
+        if ref_fx is not None:
+            rr = min(reps, 64 if batch < 64 else 8)
+            ref_fx.small_batch(ds.queries[:batch], k, p)
+            lat_r = []
+            for j in range(rr):
+                t = time.perf_counter()
+                r_ids, _, _ = ref_fx.small_batch(ds.queries[j * batch:(j + 1) * batch], k, p)
+                lat_r.append(time.perf_counter() - t)
+                assert np.array_equal(r_ids, dev_ids[j * batch:(j + 1) * batch]), "reference differs"
+            mr = float(np.median(lat_r))
+            row["reference"] = {"latency_us_p50": mr * 1e6, "qps": batch / mr,
+                                "cores": ref_fx.ref.so.ref_num_threads(), "calls": rr,
+                                "ids_equal": True}
+        out.append(row)
+    return {"procedure": "greedy (paper Alg. 1), deterministic, C2 index, hop_limit 16, lambda_cut 10",
+            "t0_rule": "cheapest t0 in (8, 10, 12, 16) with recall@10 >= 0.95 on 2000 queries",
+            "t0_recall_sweep": {str(t): v for t, v in sweep.items()}, "points": out}
+
+
+def _native_lib():
+    from paper_2204_00824_b200 import _native
+    return _native.lib()
+
+
+def _native_check(rc):
+    from paper_2204_00824_b200 import _native
+    _native.check(rc)
 
 
 def sharded_section(args, ws, rank, local, dev, dist):
@@ -338,7 +425,7 @@ def reference_inputs(name: str):
 
 def bench_config(ws: int, scaling: str) -> dict:
     """The `config` object, identical on both arms."""
-    per_gpu = 10000 if scaling == "weak" else -(-10000 // ws)
+    per_gpu = 10000 if scaling == "weak" else 10000 // ws
     return {"workload": WORKLOAD, "params": PARAMS, "scaling": scaling,
             "queries_per_gpu": per_gpu, "global_batch": 10000 * ws if scaling == "weak" else 10000,
             "parallelism": f"replicated index, {'each rank its own 10K batch' if scaling == 'weak' else 'the 10K batch split'} x{ws}"}
@@ -496,8 +583,8 @@ def main():
     p = BestFirstParams(**PARAMS)
     k = p.k
     if args.scaling == "strong":  # this rank's contiguous slice of the one 10K batch
-        per = -(-ds.queries.shape[0] // ws)
-        lo, hi = min(rank * per, ds.queries.shape[0]), min((rank + 1) * per, ds.queries.shape[0])
+        from paper_2204_00824_b200 import shards
+        lo, hi = shards.query_slice(ds.queries.shape[0], ws, rank)  # gloo-tested split
         queries, gt, qbase = ds.queries[lo:hi], ds.gt[lo:hi], lo
         total_q = ds.queries.shape[0]
     else:  # every rank its own 10K batch, RNG streams continued (query_index_base)
@@ -614,7 +701,15 @@ def main():
         del flush
         torch.cuda.empty_cache()
         if rank == 0:
-            extras["small_batch"] = small_batch_section(idx, ds, dev)
+            ref_fx = None
+            if ws == 1 and not args.no_cpu_baseline:
+                try:
+                    from oracle import oracle as O
+                    ref_fx = O.Ref().fixture(ds.graph_path, ds.base)
+                except Exception:  # reference not built on this host
+                    ref_fx = None
+            extras["small_batch"] = small_batch_section(idx, ds, dev, ref_fx)
+            del ref_fx
         extras["sharded"] = sharded_section(args, ws, rank, local, dev, dist)
         if rank == 0:
             idx.close()

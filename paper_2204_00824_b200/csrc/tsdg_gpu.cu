@@ -150,6 +150,9 @@ struct tsdg_gpu_index {
     uint32_t* counters = nullptr;  // work counters, one per launch slot (never reset:
     uint32_t counter_slot = 0;     // each launch starts from the slot's known value)
     uint32_t counter_val[64] = {};
+    cudaEvent_t slot_done[64] = {};        // recorded after each launch on a slot
+    cudaStream_t slot_stream[64] = {};     // the stream of that launch
+    bool slot_used[64] = {};
     std::map<uint32_t, uint32_t*> degcut;
     std::mutex mu;
     cudaStream_t stream = nullptr;   // for the host-pointer entry points
@@ -166,18 +169,31 @@ constexpr uint32_t kCounterSlots = 64;
 // Work-queue tickets without a memset per launch: a persistent kernel hands out work
 // with atomicAdd on its slot and every warp exits after exactly one fetch past the
 // end, so a launch advances the slot by (work items + warps).  The kernel subtracts
-// the slot's value at launch time (`base`).
+// the slot's value at launch time (`base`).  Callers hold idx->mu.
+//  - A slot is reused only after its previous launch: a launch on another stream
+//    first waits on the event recorded after that launch (same stream: in order), so
+//    any number of in-flight launches over any streams never share a live counter.
+//  - The host value advances only when the launch was accepted; a rejected launch
+//    (bad configuration, no kernel image, ...) never ran and left the word as it was.
 struct Ticket {
     uint32_t* ptr;
     uint32_t base;
     uint32_t slot;
 };
-Ticket next_counter(tsdg_gpu_index* idx) {
+Ticket next_counter(tsdg_gpu_index* idx, cudaStream_t st) {
+    (void)cudaGetLastError();  // commit_counter reads the launch's own status
     const uint32_t slot = idx->counter_slot++ % kCounterSlots;
+    if (idx->slot_used[slot] && idx->slot_stream[slot] != st)
+        cuda_check(cudaStreamWaitEvent(st, idx->slot_done[slot], 0), "cudaStreamWaitEvent(slot)");
     return Ticket{idx->counters + slot, idx->counter_val[slot], slot};
 }
-void commit_counter(tsdg_gpu_index* idx, const Ticket& t, uint64_t items, uint64_t warps) {
+void commit_counter(tsdg_gpu_index* idx, const Ticket& t, uint64_t items, uint64_t warps,
+                    cudaStream_t st) {
+    if (cudaPeekAtLastError() != cudaSuccess) return;  // not launched: word unchanged
     idx->counter_val[t.slot] += (uint32_t)(items + warps);
+    cuda_check(cudaEventRecord(idx->slot_done[t.slot], st), "cudaEventRecord(slot)");
+    idx->slot_stream[t.slot] = st;
+    idx->slot_used[t.slot] = true;
 }
 
 // Cached per-(kernel, device) launch attributes: the host side of a small-batch call
@@ -344,7 +360,7 @@ void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_dists = d_dists;
     a.out_counts = d_counts;
     a.out_stats = d_stats;
-    const Ticket tk = next_counter(idx);
+    const Ticket tk = next_counter(idx, st);
     a.work_counter = tk.ptr;
     a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
@@ -383,7 +399,7 @@ void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     else kern = fast ? bf_unbounded_kernel<2, true> : bf_unbounded_kernel<2, false>;
     set_smem(reinterpret_cast<const void*>(kern), a.warp_smem, "cudaFuncSetAttribute(unbounded)");
     kern<<<warps, 32, a.warp_smem, st>>>(a);
-    commit_counter(idx, tk, nq, warps);
+    commit_counter(idx, tk, nq, warps, st);
     g_launches++;
     cuda_check(cudaGetLastError(), "bf_unbounded_kernel launch");
     int h_over = 0;
@@ -422,7 +438,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.out_dists = d_dists;
     a.out_counts = d_counts;
     a.out_stats = d_stats;
-    const Ticket tk = next_counter(idx);
+    const Ticket tk = next_counter(idx, st);
     a.work_counter = tk.ptr;
     a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
@@ -446,7 +462,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast)");
         const int grid = grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, kFastWarps);
         kern<<<grid, kFastWarps * 32, smem, st>>>(a);
-        commit_counter(idx, tk, nq, (uint64_t)grid * kFastWarps);
+        commit_counter(idx, tk, nq, (uint64_t)grid * kFastWarps, st);
         g_launches++;
         cuda_check(cudaGetLastError(), "bf_fast_kernel launch");
         return;
@@ -459,7 +475,7 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf)");
     const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq, wpc);
     kern<<<grid, wpc * 32, smem, st>>>(a);
-    commit_counter(idx, tk, nq, (uint64_t)grid * wpc);
+    commit_counter(idx, tk, nq, (uint64_t)grid * wpc, st);
     g_launches++;
     cuda_check(cudaGetLastError(), "bf_kernel launch");
 }
@@ -518,7 +534,7 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.walk_dists = wb.dists;
     a.walk_hops = wb.hops;
     a.walk_evals = wb.evals;
-    const Ticket tk = next_counter(idx);
+    const Ticket tk = next_counter(idx, st);
     a.work_counter = tk.ptr;
     a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
@@ -543,7 +559,7 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(greedy)");
     const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq * t0, wpc);
     kern<<<grid, wpc * 32, smem, st>>>(a);
-    commit_counter(idx, tk, (uint64_t)nq * t0, (uint64_t)grid * wpc);
+    commit_counter(idx, tk, (uint64_t)nq * t0, (uint64_t)grid * wpc, st);
     g_launches++;
     cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
 }
@@ -1065,6 +1081,8 @@ void free_index(tsdg_gpu_index* idx) {
     cudaFree(idx->lam);
     cudaFree(idx->deg_full);
     cudaFree(idx->counters);
+    for (auto& e : idx->slot_done)
+        if (e) cudaEventDestroy(e);
     if (idx->stream) cudaStreamDestroy(idx->stream);
     if (idx->stream2) cudaStreamDestroy(idx->stream2);
     delete idx;
@@ -1093,6 +1111,8 @@ void init_index_runtime(tsdg_gpu_index* idx, int device) {
     }
     cuda_check(cudaMalloc(&idx->counters, kCounterSlots * 4), "cudaMalloc(counters)");
     cuda_check(cudaMemset(idx->counters, 0, kCounterSlots * 4), "cudaMemset(counters)");
+    for (auto& e : idx->slot_done)
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(slot)");
 }
 
 // File byte ranges -> device, through two pinned staging buffers: the read of

@@ -269,6 +269,32 @@ int main() {
         std::remove(gp.c_str());
         std::remove(vp.c_str());
     }
+    {
+        CASE("reference-signature free functions reuse one resident index (no re-upload per call)");
+        auto [base, queries] = make_synthetic_split(3000, 80, 16, 6, 0.25f, 93);
+        const TsdgGraph g = build(base, brute_force_knn(base, 20, Metric::L2), {1.2f, 9, 0}, Metric::L2);
+        BestFirstParams p;
+        p.k = 10;
+        p.seed = 7;
+        GreedyParams gp;
+        gp.t0 = 4;
+        const auto want_bf = large_batch_search(g, base, queries, p);
+        const auto want_gr = small_batch_search(g, base, queries, 10, gp);
+        const std::uint64_t before = gpu::index_uploads();
+        for (int rep = 0; rep < 5; ++rep) {  // bench.cpp:329,333 call once per chunk
+            CHECK(gpu::large_batch_search(g, base, queries, p) == want_bf);
+            CHECK(gpu::small_batch_search(g, base, queries, 10, gp) == want_gr);
+        }
+        CHECK(gpu::index_uploads() == before + 1);
+        // a different base (same graph object) is a different index
+        VectorSet other = base;
+        CHECK(gpu::large_batch_search(g, other, queries, p) == want_bf);
+        CHECK(gpu::index_uploads() == before + 2);
+        gpu::release_resident_indexes();
+        CHECK(gpu::large_batch_search(g, base, queries, p) == want_bf);
+        CHECK(gpu::index_uploads() == before + 3);
+        gpu::release_resident_indexes();
+    }
     std::printf("gpu_api: %d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;
 }

@@ -234,3 +234,45 @@ def test_zero_copy_greedy_equals_copy_path(fixtures, index, monkeypatch):
         np.testing.assert_array_equal(hi.numpy().view(np.uint32), want.ids)
         np.testing.assert_array_equal(hd.numpy().view(np.uint32), want.dists.view(np.uint32))
         np.testing.assert_array_equal(hc.numpy().view(np.uint32), want.counts)
+
+
+def test_many_overlapping_device_launches_on_two_streams(fixtures, index):
+    """More in-flight *_device launches than work-counter slots (64), alternating over
+    two streams with mixed procedures: every launch's results equal its own
+    synchronous search (no two live launches share a work counter)."""
+    import torch
+    from paper_2204_00824_b200.search import BestFirstParams, GreedyParams
+    g, b, q = fixtures("lowlid3k")
+    idx = index("lowlid3k")
+    p = BestFirstParams(k=10, seed=4)
+    gp = GreedyParams(t0=4, seed=4)
+    nq = q.shape[0]
+    dq = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    n_launch = 100
+    for i in range(n_launch):
+        lo = (i * 37) % (nq - 40)
+        cnt = 8 + (i * 13) % 32
+        ids = torch.full((cnt, 10), -1, dtype=torch.int32, device="cuda")
+        dd = torch.empty((cnt, 10), dtype=torch.float32, device="cuda")
+        cc = torch.empty(cnt, dtype=torch.int32, device="cuda")
+        st = streams[i % 2]
+        qp = dq[lo].data_ptr()
+        if i % 3 == 2:
+            idx.search_greedy_device(qp, cnt, 10, gp, ids.data_ptr(), dd.data_ptr(), cc.data_ptr(),
+                                     0, st.cuda_stream)
+        else:
+            idx.search_bestfirst_device(qp, cnt, p, ids.data_ptr(), dd.data_ptr(), cc.data_ptr(),
+                                        0, st.cuda_stream, query_index_base=lo,
+                                        mode=_native.MODE_FAST if i % 2 else _native.MODE_DETERMINISTIC)
+        outs.append((i, lo, cnt, ids, dd))
+    torch.cuda.synchronize()
+    for i, lo, cnt, ids, dd in outs:
+        if i % 3 == 2:
+            want = idx.search_greedy(q[lo:lo + cnt], 10, gp)
+        else:
+            want = idx.search_bestfirst(q[lo:lo + cnt], p, query_index_base=lo,
+                                        mode=_native.MODE_FAST if i % 2 else _native.MODE_DETERMINISTIC)
+        np.testing.assert_array_equal(ids.cpu().numpy().view(np.uint32), want.ids, err_msg=str(i))
+        np.testing.assert_array_equal(dd.cpu().numpy().view(np.uint32), want.dists.view(np.uint32))

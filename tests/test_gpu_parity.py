@@ -296,10 +296,12 @@ def test_fast_mode_recall_within_half_point(fixtures, index, golden, golden_meta
             r_ref = O.recall_at_k(ref_ids, ref_cnt, gt, min(10, p.k))
             r_fast = O.recall_at_k(fast.ids, fast.counts, gt, min(10, p.k))
             assert abs(r_fast - r_ref) <= 0.005, (name, i, r_fast, r_ref)
-        gp = GreedyParams(t0=8, seed=5)
-        fg = idx.search_greedy(q, 10, gp, mode=_native.MODE_FAST)
-        r_ref = O.recall_at_k(golden[f"{name}_gr0_ids"], golden[f"{name}_gr0_counts"], gt, 10)
-        assert O.recall_at_k(fg.ids, fg.counts, gt, 10) >= r_ref - 0.02
+        gd = golden_meta["gr_grid"][0]  # the params golden gr0 was produced with
+        gp = GreedyParams(**{kk: v for kk, v in gd.items() if kk != "k"})
+        fg = idx.search_greedy(q, gd["k"], gp, mode=_native.MODE_FAST)
+        for kk in (1, 10):  # north star: recall@1 / @10 within 0.5 pt
+            r_ref = O.recall_at_k(golden[f"{name}_gr0_ids"], golden[f"{name}_gr0_counts"], gt, kk)
+            assert abs(O.recall_at_k(fg.ids, fg.counts, gt, kk) - r_ref) <= 0.005, (name, kk)
 
 
 @pytest.mark.skipif(not datasets.available("c1_lowlid_100k"), reason="data/c1_lowlid_100k absent")
