@@ -167,9 +167,9 @@ def small_batch_section(idx, ds, dev, ref_fx=None):
     1 / 8 / 64, at the cheapest t0 whose recall@10 reaches 0.95 (the reference's
     small_batch_search gives the same ids: deterministic mode is bit-exact).
       device:  launch path, queries resident in HBM, CUDA events around each call
-      e2e:     the persistent server (tsdg_gpu_server_search) with pinned HOST query /
-               result buffers, wall clock around each synchronous call
-      launch:  the host-pointer launch call (tsdg_gpu_search_greedy), wall clock
+      e2e:     the host-pointer C-ABI call (tsdg_gpu_search_greedy) with pinned HOST
+               query / result buffers (zero-copy: the kernel reads the queries from and
+               writes the results to host memory), wall clock around each synchronous call
       reference: the reference's small_batch_search (oracle/_ref, all host threads)
                on the same queries, wall clock per call"""
     import torch
@@ -217,28 +217,11 @@ def small_batch_section(idx, ds, dev, ref_fx=None):
         row["device"] = {"latency_us_p50": lat * 1e3, "latency_us_p99": float(np.percentile(times, 99)) * 1e3,
                          "qps": batch / lat * 1e3}
         dev_ids = ids.cpu().numpy().view(np.uint32).copy()
-        # end to end with host buffers: the resident server, then the launch call
+        # end to end with host buffers through the reference-facing C-ABI call
         hq = torch.from_numpy(ds.queries[:nq].copy()).pin_memory()
         hi = torch.empty((nq, k), dtype=torch.int32).pin_memory()
         hd = torch.empty((nq, k), dtype=torch.float32).pin_memory()
         hc = torch.empty(nq, dtype=torch.int32).pin_memory()
-        with idx.greedy_server(k, p, max_batch=batch) as sv:
-            def scall(j):
-                o = j * batch
-                sv.search_into(hq[o].data_ptr(), batch, hi[o].data_ptr(), hd[o].data_ptr(), hc[o].data_ptr())
-            for j in range(5):
-                scall(j)
-            lat_s = []
-            for j in range(reps):
-                t = time.perf_counter()
-                scall(j)
-                lat_s.append(time.perf_counter() - t)
-        assert np.array_equal(hi.numpy().view(np.uint32), dev_ids), "server result differs"
-        m = float(np.median(lat_s))
-        row["e2e"] = {"path": "persistent server (tsdg_gpu_server_search), pinned host buffers",
-                      "latency_us_p50": m * 1e6, "latency_us_p99": float(np.percentile(lat_s, 99)) * 1e6,
-                      "qps": batch / m, "h2d_bytes_per_call": batch * ds.queries.shape[1] * 4,
-                      "d2h_bytes_per_call": batch * (k * 8 + 4)}
         L = _native_lib()
         pc = p.c()
 
@@ -252,11 +235,16 @@ def small_batch_section(idx, ds, dev, ref_fx=None):
         for j in range(3):
             lcall(j)
         lat_l = []
-        for j in range(min(reps, 128)):
+        for j in range(reps):
             t = time.perf_counter()
             lcall(j)
             lat_l.append(time.perf_counter() - t)
-        row["launch_host_call_us_p50"] = float(np.median(lat_l)) * 1e6
+        assert np.array_equal(hi.numpy().view(np.uint32), dev_ids), "e2e result differs"
+        m = float(np.median(lat_l))
+        row["e2e"] = {"path": "tsdg_gpu_search_greedy, pinned host buffers (zero-copy)",
+                      "latency_us_p50": m * 1e6, "latency_us_p99": float(np.percentile(lat_l, 99)) * 1e6,
+                      "qps": batch / m, "h2d_bytes_per_call": batch * ds.queries.shape[1] * 4,
+                      "d2h_bytes_per_call": batch * (k * 8 + 4)}
         if ref_fx is not None:
             rr = min(reps, 64 if batch < 64 else 8)
             ref_fx.small_batch(ds.queries[:batch], k, p)

@@ -13,6 +13,7 @@
 //   tsdg::small_batch_search  greedy_search.hpp:55-60     -> tsdg::gpu::small_batch_search
 //   tsdg::ground_truth        bench.cpp:35-57             -> tsdg::gpu::ground_truth
 //   tsdg::brute_force_knn     knn_graph.cpp:64-86         -> tsdg::gpu::brute_force_knn
+//   tsdg::nn_descent          knn_graph.cpp:141-251       -> tsdg::gpu::nn_descent
 //   tsdg::build               diversify.cpp:152-209       -> tsdg::gpu::build
 // with the same argument meaning, the same results (bit-exact in Mode::Deterministic)
 // and the same exception types (std::invalid_argument / std::runtime_error).
@@ -433,6 +434,28 @@ inline KnnGraph brute_force_knn(const VectorSet& set, std::uint32_t k, Metric me
     std::uint32_t k_eff = 0;
     check(tsdg_gpu_brute_force_knn(set.data.data(), set.n, set.d, k, static_cast<int>(metric),
                                    device, ids.data(), dists.data(), &k_eff));
+    KnnGraph g;
+    g.n = set.n;
+    g.k = k_eff;
+    g.flat.resize(ids.size());
+    for (std::size_t i = 0; i < ids.size(); ++i) g.flat[i] = {ids[i], dists[i]};
+    return g;
+}
+
+/// tsdg::nn_descent (knn_graph.cpp:141-251): the same KnnGraph bit for bit for the same
+/// (k, metric, iterations, sample_rate, seed).  Errors as the reference
+/// (std::invalid_argument); k is clamped to n-1 with the reference's warning.
+inline KnnGraph nn_descent(const VectorSet& set, std::uint32_t k, Metric metric,
+                           std::uint32_t iterations, double sample_rate, std::uint64_t rng_seed,
+                           int device = 0) {
+    require_metric_ready(set, metric);
+    const std::uint32_t kk = set.n >= 2 ? std::max(1u, std::min(k, set.n - 1)) : 1u;
+    std::vector<std::uint32_t> ids(static_cast<std::size_t>(set.n) * kk);
+    std::vector<float> dists(ids.size());
+    std::uint32_t k_eff = 0;
+    check(tsdg_gpu_nn_descent(set.data.data(), set.n, set.d, k, static_cast<int>(metric),
+                              iterations, sample_rate, rng_seed, device, ids.data(), dists.data(),
+                              &k_eff, nullptr));
     KnnGraph g;
     g.n = set.n;
     g.k = k_eff;

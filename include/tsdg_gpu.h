@@ -173,21 +173,6 @@ int tsdg_gpu_greedy_once(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
                          const uint64_t* rng_states, uint32_t hop_limit, uint32_t lambda_cut,
                          uint32_t* ids32, float* dists32, tsdg_query_stats* stats);
 
-/* ---- persistent small-batch server (small_batch_search, greedy_search.cpp:106-127)
- * The latency form of tsdg_gpu_search_greedy: the cluster-per-query kernel stays
- * resident on the GPU and is fed through mapped pinned host memory, so a request
- * costs no kernel launch, copy or stream synchronisation (the calling thread spins
- * on the response word).  Same results as tsdg_gpu_search_greedy with the same
- * (k, params, mode).  Limits: t0 <= 16, k <= 64, nq <= max_batch per request; the
- * server occupies min(max_batch, co-resident clusters) x t0 CTAs until destroyed.
- * Requests on one server are serialised (internal mutex). */
-typedef struct tsdg_gpu_server tsdg_gpu_server;
-int tsdg_gpu_server_create(tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* params,
-                           int mode, uint32_t max_batch, tsdg_gpu_server** out);
-int tsdg_gpu_server_search(tsdg_gpu_server* server, const float* queries, uint32_t nq,
-                           uint32_t* ids, float* dists, uint32_t* counts);
-int tsdg_gpu_server_info(const tsdg_gpu_server* server, uint32_t* clusters, uint32_t* max_batch);
-int tsdg_gpu_server_destroy(tsdg_gpu_server* server);
 
 /* ---- sharded base: per-shard top-k merge (no reference counterpart) ----------
  * After an all-gather of S shards' results (each nq x k, LOCAL ids, ascending),
@@ -262,6 +247,17 @@ int tsdg_gpu_exact_topk_device(const float* d_base, uint32_t n, uint32_t ld_base
                                const float* d_queries, uint32_t nq, uint32_t ld_queries,
                                uint32_t d, uint32_t k, int metric, int exclude_self,
                                uint64_t self_base, uint32_t* d_ids, float* d_dists, void* stream);
+
+/* tsdg_gpu_nn_descent replaces tsdg::nn_descent (knn_graph.cpp:141-251): the same
+ * KnnGraph bit for bit (ids and fp32 distances, rows ascending by (dist, id)) for the
+ * same (set, k, metric, iterations, sample_rate, seed), independent of scheduling as
+ * the reference's is of its thread count.  Errors as the reference: sample_rate outside
+ * (0, 1], n < 2 and k < 1 are invalid; k > n-1 is clamped to n-1 (warning on stderr)
+ * and returned in *k_eff.  GPU limits: k_eff <= 128, n < 2^31.  stats4 (nullable) =
+ * {offers merged, join chunks, chunk re-runs, kernel launches}. */
+int tsdg_gpu_nn_descent(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                        uint32_t iterations, double sample_rate, uint64_t seed, int device,
+                        uint32_t* ids, float* dists, uint32_t* k_eff, uint64_t* stats4);
 
 /* ---- GPU two-stage diversification ------------------------
  * Replaces tsdg::build (diversify.cpp:152-209): stage 1 relaxed GD per node

@@ -31,7 +31,7 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-GPU_SRCS = ("tsdg_gpu.cu", "bf_fast.cu", "tsdg_io.cpp")
+GPU_SRCS = ("tsdg_gpu.cu", "bf_fast.cu", "nndescent.cu", "tsdg_io.cpp")
 
 
 def _build_so(out: str, extra: list, force: bool) -> str:

@@ -62,15 +62,13 @@ SIGNATURES = {
     "tsdg_gpu_search_greedy_device": (_I, [_VP, _VP, _U32, _U32, _VP, _I, _VP, _VP, _VP, _VP,
                                            _VP]),
     "tsdg_gpu_greedy_once": (_I, [_VP, _VP, _U32, _VP, _U32, _U32, _VP, _VP, _VP]),
-    "tsdg_gpu_server_create": (_I, [_VP, _U32, _VP, _I, _U32, _VP]),
-    "tsdg_gpu_server_search": (_I, [_VP, _VP, _U32, _VP, _VP, _VP]),
-    "tsdg_gpu_server_info": (_I, [_VP, _VP, _VP]),
-    "tsdg_gpu_server_destroy": (_I, [_VP]),
     "tsdg_gpu_merge_shards_device": (_I, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _VP, _VP, _VP,
                                           _VP]),
     "tsdg_gpu_ground_truth": (_I, [_VP, _U32, _VP, _U32, _U32, _U32, _I, _I, _VP, _VP]),
     "tsdg_gpu_index_ground_truth": (_I, [_VP, _VP, _U32, _U32, _VP, _VP]),
     "tsdg_gpu_brute_force_knn": (_I, [_VP, _U32, _U32, _U32, _I, _I, _VP, _VP, _VP]),
+    "tsdg_gpu_nn_descent": (_I, [_VP, _U32, _U32, _U32, _I, _U32, ctypes.c_double, _U64, _I,
+                                 _VP, _VP, _VP, _VP]),
     "tsdg_gpu_exact_topk_device": (_I, [_VP, _U32, _U32, _VP, _U32, _U32, _U32, _U32, _I, _I,
                                         _U64, _VP, _VP, _VP]),
     "tsdg_gpu_build": (_I, [_VP, _U32, _U32, _VP, _VP, _U32, _F, ctypes.c_uint16, _U32, _I, _I,

@@ -4,14 +4,15 @@ the same sweep expansion and auto routing, the same per-chunk seeding
 (bp.seed = mix64(seed + begin), bench.cpp:331-333), the same recall (bench.cpp:59-78)
 and the same CSV (write_bench_csv, bench.cpp:177-187).  Every piece of work runs on
 the B200: ground truth by the exact scan, the graph (when not loaded) by the GPU
-brute-force k-NN + two-stage diversification, the searches by the best-first /
+brute-force k-NN or nn_descent + two-stage diversification, the searches by the best-first /
 greedy kernels (deterministic mode by default: the same traversal, so recall,
 mean_hops and mean_distance_evals equal the reference's row for row).
 
     python -m paper_2204_00824_b200.bench_runner config.json [out.csv] [--fast]
 
-Not on the GPU: graph method "nndescent" (knn_graph.cpp:141-251) — pass a prebuilt
-"tsdg" graph (e.g. from the reference's `tsdg diversify`) instead.
+Graph method "nndescent" (bench.cpp:245-247, keys iterations / sample_rate / knn_seed
+with the reference's defaults 10 / 1.0 / 7) runs the GPU nn_descent, which returns the
+reference's KnnGraph bit for bit.
 """
 from __future__ import annotations
 
@@ -29,7 +30,7 @@ import numpy as np
 from . import _native, datasets
 from .search import (BestFirstParams, GpuIndex, GreedyParams, InvalidArgument, KnnGraph,
                      SearchStats, TsdgRuntimeError, brute_force_knn, build, ground_truth,
-                     load_tsdg)
+                     load_tsdg, nn_descent)
 
 METRIC_NAMES = {0: "l2", 1: "cos", 2: "ip"}
 
@@ -227,10 +228,13 @@ def run_bench_file(config_path: str, csv_out: str = "", device: int = 0,
         if graph.metric != metric:
             raise TsdgRuntimeError("bench: graph metric does not match dataset metric")
     else:
+        knn_k = int(gcfg.get("knn_k", 100))
         if gcfg.get("method", "brute") == "nndescent":
-            raise TsdgRuntimeError("bench: graph method 'nndescent' is not implemented on the "
-                                   "GPU; build the graph with the reference and pass 'tsdg'")
-        knn = brute_force_knn(base, int(gcfg.get("knn_k", 100)), metric, device)
+            knn = nn_descent(base, knn_k, int(gcfg.get("iterations", 10)),
+                             float(gcfg.get("sample_rate", 1.0)), int(gcfg.get("knn_seed", 7)),
+                             metric, device)
+        else:
+            knn = brute_force_knn(base, knn_k, metric, device)
         graph = build(base, knn, float(gcfg.get("alpha", 1.2)), int(gcfg.get("lambda0", 9)),
                       int(gcfg.get("max_degree", 0)), metric, device)
     threshold = int(cfg.get("routing", {}).get("small_batch_threshold", 256))

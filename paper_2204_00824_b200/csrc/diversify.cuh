@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kDivThreads, 2) div_stage1_kernel(const DivArg
 }
 
 // ---- reverse edges ---------------------------------------------------------------
-__global__ void div_rev_count_kernel(const DivArgs a, uint32_t* rev_cnt) {
+static __global__ void div_rev_count_kernel(const DivArgs a, uint32_t* rev_cnt) {
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t u = (uint32_t)(t / a.k), j = (uint32_t)(t % a.k);
     if (u >= a.n || j >= a.s1_cnt[u]) return;
@@ -220,7 +220,7 @@ __global__ void div_rev_count_kernel(const DivArgs a, uint32_t* rev_cnt) {
 
 // forward entries first (stage-1 order), reverse entries appended (order fixed later
 // by the dedup + (dist, target) ranking, so the atomic append order does not matter)
-__global__ void div_fill_kernel(const DivArgs a, uint32_t* cursor) {
+static __global__ void div_fill_kernel(const DivArgs a, uint32_t* cursor) {
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t u = (uint32_t)(t / a.k), j = (uint32_t)(t % a.k);
     if (u >= a.n || j >= a.s1_cnt[u]) return;
@@ -236,7 +236,7 @@ __global__ void div_fill_kernel(const DivArgs a, uint32_t* cursor) {
 
 // sort by (target, dist) + unique by target (diversify.cpp:101-110): entry j survives
 // iff no other entry has its target with a smaller (dist, index).  Warp per node.
-__global__ void div_dedup_kernel(const DivArgs a) {
+static __global__ void div_dedup_kernel(const DivArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (u >= a.n) return;

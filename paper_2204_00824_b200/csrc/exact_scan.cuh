@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
 
 // Per query, merge S sorted split lists (disjoint row ranges) into the first k by
 // (dist, id).  One warp per query; lane s < S tracks list s.
-__global__ void merge_splits_kernel(const uint32_t* in_ids, const float* in_dists, uint32_t S,
+static __global__ void merge_splits_kernel(const uint32_t* in_ids, const float* in_dists, uint32_t S,
                                     uint32_t nq, uint32_t k, uint32_t* out_ids, float* out_dists) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);

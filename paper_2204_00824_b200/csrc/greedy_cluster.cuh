@@ -76,8 +76,8 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-// Output targets of one query (the launch path: the result arrays; the server:
-// mapped host memory).
+// Output targets of one query (device memory, or mapped host memory on the
+// zero-copy host-pointer path).
 struct GcOut {
     uint32_t* ids;  // k entries for this query
     float* dists;   // or nullptr
@@ -114,7 +114,7 @@ __device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_r
 
 // One walk (CTA) of query q: select_start + hops + (cluster mode) the in-cluster merge
 // of the t0 walks into `o`.  gq: the query (any memory space the SM can read: device
-// memory, or mapped host memory for the server); s: the walk's RNG stream index.
+// memory, or mapped host memory); s: the walk's RNG stream index.
 template <int METRIC, bool FAST, int STAGE>
 __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpStage& w,
                                          uint32_t s, uint32_t walk, const float* gq,

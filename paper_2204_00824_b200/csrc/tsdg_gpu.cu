@@ -32,8 +32,9 @@
 #include "bf_fast.cuh"
 #include "diversify.cuh"
 #include "exact_scan.cuh"
-#include "greedy_server.cuh"
+#include "greedy_cluster.cuh"
 #include "loader.cuh"
+#include "nndescent.h"
 #include "unbounded.cuh"
 
 using namespace tsdg_dev;
@@ -117,25 +118,6 @@ struct tsdg_gpu_sharded {
     std::vector<tsdg_gpu_index*> shards;
     std::vector<uint64_t> offsets;
     uint32_t d = 0;
-};
-
-// Persistent small-batch server (greedy_server.cuh): mapped request / response
-// buffers and the resident cluster kernel's stream.
-struct tsdg_gpu_server {
-    tsdg_gpu_index* idx = nullptr;
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    unsigned char* host = nullptr;  // one mapped pinned allocation
-    tsdg_dev::GsReq* req = nullptr;
-    tsdg_dev::GsResp* resp = nullptr;
-    float* req_q = nullptr;
-    uint32_t* resp_ids = nullptr;
-    float* resp_dists = nullptr;
-    uint32_t* resp_counts = nullptr;
-    uint32_t* dev_words = nullptr;  // dev_seq, dev_done
-    uint32_t seq = 0, k = 0, d = 0, max_batch = 0, nclusters = 0;
-    bool failed = false;
-    std::mutex mu;
 };
 
 struct tsdg_gpu_index {
@@ -566,7 +548,7 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
 
 // CTA-per-walk / cluster-per-query greedy (greedy_cluster.cuh).  Returns false when
 // the cluster launch is not possible (then the caller merges walks itself).
-// GcArgs + shared-memory carve of the CTA-per-walk kernels (launch path and server).
+// GcArgs + shared-memory carve of the CTA-per-walk kernels.
 size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* p,
                     bool cluster, cudaStream_t st) {
     a.vec = idx->vec;
@@ -1697,150 +1679,6 @@ int tsdg_gpu_search_greedy(tsdg_gpu_index* idx, const float* queries, uint32_t n
     });
 }
 
-int tsdg_gpu_server_create(tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* params,
-                           int mode, uint32_t max_batch, tsdg_gpu_server** out) {
-    return guarded([&] {
-        if (!out) fail(TSDG_EINVAL, "server_create: null out");
-        *out = nullptr;
-        if (!idx) fail(TSDG_EINVAL, "server_create: null index");
-        validate_greedy(idx, k, params);
-        if (params->t0 > 16) fail(TSDG_EINVAL, "server: t0 <= 16 (one thread-block cluster per query)");
-        if (k > 64) fail(TSDG_EINVAL, "server: k <= 64");
-        if (max_batch < 1) fail(TSDG_EINVAL, "server: max_batch must be >= 1");
-        std::lock_guard<std::mutex> lk(idx->mu);
-        DeviceGuard dg(idx->device);
-        auto sv = std::make_unique<tsdg_gpu_server>();
-        sv->idx = idx;
-        sv->device = idx->device;
-        sv->k = k;
-        sv->d = idx->d;
-        sv->max_batch = max_batch;
-        GsArgs sa{};
-        const size_t smem = fill_gc_args(sa.a, idx, k, params, true, idx->stream);
-        cuda_check(cudaStreamSynchronize(idx->stream), "server_create");
-        void (*kern)(GsArgs);
-        const bool fast = mode == TSDG_MODE_FAST;
-        if (idx->metric == 0) kern = fast ? greedy_server_kernel<0, true> : greedy_server_kernel<0, false>;
-        else if (idx->metric == 1) kern = fast ? greedy_server_kernel<1, true> : greedy_server_kernel<1, false>;
-        else kern = fast ? greedy_server_kernel<2, true> : greedy_server_kernel<2, false>;
-        set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(server)");
-        if (params->t0 > 8)
-            cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                       "cudaFuncSetAttribute(non-portable cluster)");
-        cudaLaunchConfig_t cfg{};
-        cfg.blockDim = dim3(kGcThreads);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = params->t0;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cfg.gridDim = dim3(params->t0);
-        int resident = 0;
-        cuda_check(cudaOccupancyMaxActiveClusters(&resident, kern, &cfg), "cudaOccupancyMaxActiveClusters");
-        if (resident < 1) fail(TSDG_ERUNTIME, "server: a cluster of t0 CTAs does not fit");
-        // every cluster must be resident at once (they never exit between requests)
-        sv->nclusters = std::min<uint32_t>(max_batch, (uint32_t)resident);
-        const size_t qb = round_up((uint32_t)((size_t)max_batch * idx->d * 4), 256);
-        const size_t ib = round_up(max_batch * k * 4, 256);
-        const size_t cb = round_up(max_batch * 4, 256);
-        const size_t total = 512 + qb + 2 * ib + cb;
-        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&sv->host), total,
-                                 cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc(server)");
-        std::memset(sv->host, 0, total);
-        sv->req = reinterpret_cast<GsReq*>(sv->host);
-        sv->resp = reinterpret_cast<GsResp*>(sv->host + 256);
-        sv->req_q = reinterpret_cast<float*>(sv->host + 512);
-        sv->resp_ids = reinterpret_cast<uint32_t*>(sv->host + 512 + qb);
-        sv->resp_dists = reinterpret_cast<float*>(sv->host + 512 + qb + ib);
-        sv->resp_counts = reinterpret_cast<uint32_t*>(sv->host + 512 + qb + 2 * ib);
-        cuda_check(cudaMalloc(&sv->dev_words, 2 * sizeof(uint32_t)), "cudaMalloc(server)");
-        cuda_check(cudaMemset(sv->dev_words, 0, 2 * sizeof(uint32_t)), "cudaMemset(server)");
-        cuda_check(cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking), "cudaStreamCreate(server)");
-        unsigned char* dhost = nullptr;
-        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhost), sv->host, 0),
-                   "cudaHostGetDevicePointer(server)");
-        sa.a.queries = nullptr;
-        sa.a.nq = 0;
-        sa.req = reinterpret_cast<const GsReq*>(dhost);
-        sa.resp = reinterpret_cast<GsResp*>(dhost + 256);
-        sa.req_queries = reinterpret_cast<const float*>(dhost + 512);
-        sa.resp_ids = reinterpret_cast<uint32_t*>(dhost + 512 + qb);
-        sa.resp_dists = reinterpret_cast<float*>(dhost + 512 + qb + ib);
-        sa.resp_counts = reinterpret_cast<uint32_t*>(dhost + 512 + qb + 2 * ib);
-        sa.nclusters = sv->nclusters;
-        sa.dev_seq = sv->dev_words;
-        sa.dev_done = sv->dev_words + 1;
-        cfg.gridDim = dim3(sv->nclusters * params->t0);
-        cfg.stream = sv->stream;
-        cuda_check(cudaLaunchKernelEx(&cfg, kern, sa), "greedy_server_kernel launch");
-        g_launches++;
-        *out = sv.release();
-    });
-}
-
-namespace {
-void server_stop(tsdg_gpu_server* sv) {
-    if (!sv->stream) return;
-    __atomic_store_n(&sv->req->stop, 1u, __ATOMIC_RELEASE);
-    cudaStreamSynchronize(sv->stream);
-}
-}  // namespace
-
-int tsdg_gpu_server_search(tsdg_gpu_server* sv, const float* queries, uint32_t nq, uint32_t* ids,
-                           float* dists, uint32_t* counts) {
-    return guarded([&] {
-        if (!sv) fail(TSDG_EINVAL, "server_search: null server");
-        if (nq == 0) return;
-        if (!queries || !ids) fail(TSDG_EINVAL, "server_search: null buffer");
-        if (nq > sv->max_batch) fail(TSDG_EINVAL, "server_search: batch larger than max_batch");
-        check_cosine_queries(sv->idx, queries, nq);
-        std::lock_guard<std::mutex> lk(sv->mu);
-        if (sv->failed) fail(TSDG_ERUNTIME, "server_search: server is not running");
-        std::memcpy(sv->req_q, queries, (size_t)nq * sv->d * 4);
-        sv->req->nq = nq;
-        const uint32_t seq = ++sv->seq;
-        __atomic_store_n(&sv->req->seq, seq, __ATOMIC_RELEASE);
-        auto t0 = std::chrono::steady_clock::now();
-        for (uint64_t spin = 0;; ++spin) {
-            if (__atomic_load_n(&sv->resp->seq, __ATOMIC_ACQUIRE) == seq) break;
-            __builtin_ia32_pause();
-            if ((spin & 0xFFFF) == 0xFFFF) {
-                const cudaError_t e = cudaStreamQuery(sv->stream);
-                const bool timeout = std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30);
-                if ((e != cudaErrorNotReady) || timeout) {
-                    sv->failed = true;
-                    fail(TSDG_ERUNTIME, std::string("server_search: server kernel ") +
-                                            (timeout ? "timed out" : cudaGetErrorString(e)));
-                }
-            }
-        }
-        std::memcpy(ids, sv->resp_ids, (size_t)nq * sv->k * 4);
-        if (dists) std::memcpy(dists, sv->resp_dists, (size_t)nq * sv->k * 4);
-        if (counts) std::memcpy(counts, sv->resp_counts, (size_t)nq * 4);
-    });
-}
-
-int tsdg_gpu_server_info(const tsdg_gpu_server* sv, uint32_t* clusters, uint32_t* max_batch) {
-    if (!sv) return TSDG_EINVAL;
-    if (clusters) *clusters = sv->nclusters;
-    if (max_batch) *max_batch = sv->max_batch;
-    return TSDG_OK;
-}
-
-int tsdg_gpu_server_destroy(tsdg_gpu_server* sv) {
-    return guarded([&] {
-        if (!sv) return;
-        DeviceGuard dg(sv->device);
-        server_stop(sv);
-        if (sv->stream) cudaStreamDestroy(sv->stream);
-        if (sv->dev_words) cudaFree(sv->dev_words);
-        if (sv->host) cudaFreeHost(sv->host);
-        delete sv;
-    });
-}
 
 int tsdg_gpu_greedy_once(tsdg_gpu_index* idx, const float* queries, uint32_t nq,
                          const uint64_t* rng_states, uint32_t hop_limit, uint32_t lambda_cut,
@@ -2000,6 +1838,64 @@ int tsdg_gpu_brute_force_knn(const float* base, uint32_t n, uint32_t d, uint32_t
     });
 }
 
+int tsdg_gpu_nn_descent(const float* base, uint32_t n, uint32_t d, uint32_t k, int metric,
+                        uint32_t iterations, double sample_rate, uint64_t seed, int device,
+                        uint32_t* ids, float* dists, uint32_t* k_eff, uint64_t* stats4) {
+    return guarded([&] {
+        if (metric < 0 || metric > 2) fail(TSDG_EINVAL, "invalid metric");
+        // knn_graph.cpp:144-146, then clamp_k (:17-26)
+        if (!(sample_rate > 0.0 && sample_rate <= 1.0))
+            fail(TSDG_EINVAL, "nn_descent: sample_rate must be in (0, 1]");
+        if (n < 2) fail(TSDG_EINVAL, "nn_descent: need at least 2 vectors");
+        if (k < 1) fail(TSDG_EINVAL, "nn_descent: k must be >= 1");
+        if (k > n - 1) {
+            std::fprintf(stderr, "nn_descent: k=%u clamped to n-1=%u\n", k, n - 1);
+            k = n - 1;
+        }
+        if (k_eff) *k_eff = k;
+        if (k > kNdMaxK) fail(TSDG_EINVAL, "nn_descent: GPU path supports k <= 128");
+        if (n > 0x7FFFFFFFu) fail(TSDG_EINVAL, "nn_descent: GPU path supports n < 2^31");
+        if (d < 1) fail(TSDG_EINVAL, "nn_descent: d must be >= 1");
+        if (!base || !ids || !dists) fail(TSDG_EINVAL, "nn_descent: null pointer");
+        // knn_graph.cpp:170-171: std::round(sample_rate * k_eff), at least 1
+        const uint32_t ms = (uint32_t)std::max(1.0, std::round(sample_rate * (double)k));
+        DeviceGuard dg(device);
+        cudaStream_t st;
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        const uint32_t ld = round_up(d, 4);
+        float* db = nullptr;
+        uint32_t* di = nullptr;
+        float* dd = nullptr;
+        auto release = [&] {
+            cudaFreeAsync(db, st);
+            cudaFreeAsync(di, st);
+            cudaFreeAsync(dd, st);
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        };
+        try {
+            db = upload_rows(base, n, d, ld, st);
+            di = dev_alloc<uint32_t>((size_t)n * k, st);
+            dd = dev_alloc<float>((size_t)n * k, st);
+            NnDescentStats ns{};
+            nn_descent_device(db, n, d, ld, k, metric, iterations, ms, seed, di, dd, st, &ns);
+            g_launches += ns.launches;
+            cuda_check(cudaMemcpyAsync(ids, di, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+            cuda_check(cudaMemcpyAsync(dists, dd, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+            cuda_check(cudaStreamSynchronize(st), "nn_descent");
+            if (stats4) {
+                stats4[0] = ns.offers;
+                stats4[1] = ns.chunks;
+                stats4[2] = ns.reruns;
+                stats4[3] = ns.launches;
+            }
+        } catch (...) {
+            release();
+            throw;
+        }
+        release();
+    });
+}
 
 // ---- GPU two-stage diversification --------------------------------------------------
 int tsdg_gpu_build(const float* base, uint32_t n, uint32_t d, const uint32_t* knn_ids,

@@ -258,11 +258,6 @@ class GpuIndex:
                                            _p(ids), _p(dists), _p(counts), _p(stats)))
         return SearchResult(ids, dists, counts, stats)
 
-    def greedy_server(self, k: int, params: GreedyParams = GreedyParams(), *,
-                      mode: int = _native.MODE_DETERMINISTIC, max_batch: int = 64) -> "GreedyServer":
-        """Persistent small-batch server over this index (tsdg_gpu_server_*)."""
-        return GreedyServer(self, k, params, mode=mode, max_batch=max_batch)
-
     def small_batch_search(self, queries, k: int, params: GreedyParams = GreedyParams(),
                            stats: Optional[SearchStats] = None, **kw) -> List[np.ndarray]:
         r = self.search_greedy(queries, k, params, **kw)
@@ -463,6 +458,26 @@ def brute_force_knn(base, k: int, metric: int = 0, device: int = 0) -> KnnGraph:
     return KnnGraph(n, int(keff.value), ids, dists)
 
 
+def nn_descent(base, k: int, iterations: int, sample_rate: float, seed: int, metric: int = 0,
+               device: int = 0, stats: Optional[dict] = None) -> KnnGraph:
+    """tsdg::nn_descent (knn_graph.cpp:141-251) on the GPU: the reference's KnnGraph
+    bit for bit for the same (k, metric, iterations, sample_rate, seed); k clamped to
+    n-1 (warning on stderr); sample_rate outside (0, 1] is an InvalidArgument."""
+    b = _f32rows(base)
+    n = b.shape[0]
+    kk = max(1, min(int(k), max(n - 1, 1)))
+    ids = np.empty((n, kk), np.uint32)
+    dists = np.empty((n, kk), np.float32)
+    keff = ctypes.c_uint32(0)
+    st = np.zeros(4, np.uint64)
+    check(lib().tsdg_gpu_nn_descent(_p(b), n, b.shape[1], int(k), int(metric), int(iterations),
+                                    float(sample_rate), int(seed) & 0xFFFFFFFFFFFFFFFF, device,
+                                    _p(ids), _p(dists), ctypes.byref(keff), _p(st)))
+    if stats is not None:
+        stats.update(offers=int(st[0]), chunks=int(st[1]), reruns=int(st[2]), launches=int(st[3]))
+    return KnnGraph(n, int(keff.value), ids, dists)
+
+
 @dataclass
 class BuildStats:
     """tsdg::BuildStats (diversify.hpp:39-44)."""
@@ -562,58 +577,6 @@ __all__ = ["BestFirstParams", "GreedyParams", "SearchStats", "SearchResult", "Ts
            "GpuIndex", "load_tsdg", "large_batch_search", "bestfirst_search",
            "small_batch_search", "small_batch_search_one", "merge_shards_device",
            "GroundTruth", "KnnGraph", "ground_truth", "exact_topk", "brute_force_knn",
-           "BuildStats", "build", "MultiGpuIndex", "ShardedGpuIndex",
+           "BuildStats", "build", "nn_descent", "MultiGpuIndex", "ShardedGpuIndex",
            "InvalidArgument", "TsdgRuntimeError", "KINVALID", "QUERY_STATS_DTYPE"]
 
-
-class GreedyServer:
-    """Resident small-batch (Alg. 1) search: the cluster-per-query kernel stays on the
-    GPU and takes requests through mapped pinned memory (tsdg_gpu_server_*), so a
-    call pays no launch or copy.  Results equal GpuIndex.search_greedy with the same
-    (k, params, mode).  Use as a context manager or call close()."""
-
-    def __init__(self, index: "GpuIndex", k: int, params: GreedyParams = GreedyParams(), *,
-                 mode: int = _native.MODE_DETERMINISTIC, max_batch: int = 64):
-        self.index, self.k, self.max_batch = index, int(k), int(max_batch)
-        self._keep = index  # the index must outlive the server
-        h = ctypes.c_void_p()
-        pc = params.c()
-        check(lib().tsdg_gpu_server_create(index._h, int(k), ctypes.byref(pc), int(mode),
-                                           self.max_batch, ctypes.byref(h)))
-        self._h = h
-        c, mb = ctypes.c_uint32(), ctypes.c_uint32()
-        check(lib().tsdg_gpu_server_info(h, ctypes.byref(c), ctypes.byref(mb)))
-        self.clusters = int(c.value)
-        self._ids = np.empty((self.max_batch, max(self.k, 1)), np.uint32)
-        self._dists = np.empty((self.max_batch, max(self.k, 1)), np.float32)
-        self._counts = np.empty(self.max_batch, np.uint32)
-
-    def search(self, queries) -> SearchResult:
-        q = _f32rows(queries, self.index.d)
-        nq = q.shape[0]
-        ids, dists, counts = self._ids[:nq], self._dists[:nq], self._counts[:nq]
-        check(lib().tsdg_gpu_server_search(self._h, _p(q), nq, _p(ids), _p(dists), _p(counts)))
-        return SearchResult(ids.copy(), dists.copy(), counts.copy(), np.zeros(nq, QUERY_STATS_DTYPE))
-
-    def search_into(self, q_ptr: int, nq: int, ids_ptr: int, dists_ptr: int, counts_ptr: int) -> None:
-        """Raw-pointer form (host buffers) for latency measurement."""
-        check(lib().tsdg_gpu_server_search(self._h, ctypes.c_void_p(q_ptr), nq,
-                                           ctypes.c_void_p(ids_ptr), ctypes.c_void_p(dists_ptr),
-                                           ctypes.c_void_p(counts_ptr)))
-
-    def close(self) -> None:
-        if getattr(self, "_h", None):
-            check(lib().tsdg_gpu_server_destroy(self._h))
-            self._h = None
-
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *exc):
-        self.close()
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass

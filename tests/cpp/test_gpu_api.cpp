@@ -270,6 +270,22 @@ int main() {
         std::remove(vp.c_str());
     }
     {
+        CASE("nn_descent == reference KnnGraph (knn_graph.cpp:141-251)");
+        auto [base, queries] = make_synthetic_split(2500, 10, 24, 7, 0.3f, 95);
+        for (double rate : {0.5, 1.0}) {
+            const KnnGraph want = nn_descent(base, 20, Metric::L2, 4, rate, 17);
+            const KnnGraph got = gpu::nn_descent(base, 20, Metric::L2, 4, rate, 17);
+            CHECK(got == want);
+        }
+        bool threw = false;
+        try {
+            gpu::nn_descent(base, 20, Metric::L2, 4, 0.0, 17);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {
         CASE("reference-signature free functions reuse one resident index (no re-upload per call)");
         auto [base, queries] = make_synthetic_split(3000, 80, 16, 6, 0.25f, 93);
         const TsdgGraph g = build(base, brute_force_knn(base, 20, Metric::L2), {1.2f, 9, 0}, Metric::L2);

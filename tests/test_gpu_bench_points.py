@@ -6,7 +6,7 @@
   EdgeTrace size on a sample); fast mode within 0.5 pt of it at recall@1 and @10
   (north star).  large_batch_search: bestfirst_search.cpp:129-150.
 - C3 (small batch on the same 1M index): greedy at t0 = 10 / 16, batches 1 / 8 / 64,
-  both Alg. 1 kernels and the persistent server, bit-exact.
+  both Alg. 1 kernels, bit-exact.
   small_batch_search: greedy_search.cpp:106-127.
 - C4 (1M x 960, 3840-B rows): best-first at the bench's k_search, bit-exact.
 - the sharded stand-in (2M x 96 in 8 shards): the device merge of the per-shard
