@@ -118,6 +118,18 @@ struct tsdg_gpu_sharded {
     std::vector<tsdg_gpu_index*> shards;
     std::vector<uint64_t> offsets;
     uint32_t d = 0;
+    // persistent workspace (grow-only, sized for nq_cap queries x k_cap results):
+    // per shard its queries and top-k on its own device, an event marking them
+    // ready; on the first shard's device the gathered [shard][query][k] block and
+    // the merged output.  Serialised by mu.
+    std::mutex mu;
+    size_t nq_cap = 0, k_cap = 0;
+    std::vector<float*> sq;
+    std::vector<uint32_t*> sid, scnt;
+    std::vector<float*> sdist;
+    std::vector<cudaEvent_t> done;
+    uint32_t *gid = nullptr, *gcnt = nullptr, *oid = nullptr, *ocnt = nullptr;
+    float *gdist = nullptr, *odist = nullptr;
 };
 
 struct tsdg_gpu_index {
@@ -1013,6 +1025,71 @@ void run_per_device(size_t ndev, F&& fn) {
     for (size_t i = 0; i < ndev; ++i)
         if (rc[i] != TSDG_OK) fail(rc[i], msg[i]);
 }
+// Sharded index workspace: release (also of a partially built index), and grow-only
+// reservation for nq queries x k results.
+void sharded_release_buffers(tsdg_gpu_sharded* sh) {
+    for (size_t i = 0; i < sh->shards.size() && i < sh->sid.size(); ++i) {
+        if (!sh->shards[i]) continue;
+        DeviceGuard dg(sh->shards[i]->device);
+        cudaStreamSynchronize(sh->shards[i]->stream);
+        cudaFree(sh->sq[i]);
+        cudaFree(sh->sid[i]);
+        cudaFree(sh->sdist[i]);
+        cudaFree(sh->scnt[i]);
+        sh->sq[i] = nullptr;
+        sh->sid[i] = sh->scnt[i] = nullptr;
+        sh->sdist[i] = nullptr;
+    }
+    if (!sh->shards.empty() && sh->shards[0]) {
+        DeviceGuard dg(sh->shards[0]->device);
+        cudaStreamSynchronize(sh->shards[0]->stream);
+        for (void* p : {(void*)sh->gid, (void*)sh->gdist, (void*)sh->gcnt, (void*)sh->oid,
+                        (void*)sh->odist, (void*)sh->ocnt})
+            cudaFree(p);
+    }
+    sh->gid = sh->gcnt = sh->oid = sh->ocnt = nullptr;
+    sh->gdist = sh->odist = nullptr;
+    sh->nq_cap = sh->k_cap = 0;
+}
+void sharded_free(tsdg_gpu_sharded* sh) {
+    sharded_release_buffers(sh);
+    for (size_t i = 0; i < sh->done.size(); ++i) {
+        if (!sh->done[i]) continue;
+        DeviceGuard dg(sh->shards[i] ? sh->shards[i]->device : 0);
+        cudaEventDestroy(sh->done[i]);
+        sh->done[i] = nullptr;
+    }
+    for (auto*& p : sh->shards) {
+        if (p) tsdg_gpu_index_destroy(p);
+        p = nullptr;
+    }
+}
+void sharded_reserve(tsdg_gpu_sharded* sh, size_t nq, size_t k) {
+    if (nq <= sh->nq_cap && k <= sh->k_cap) return;
+    const size_t nqc = std::max(nq, sh->nq_cap), kc = std::max(k, sh->k_cap);
+    sharded_release_buffers(sh);
+    const size_t S = sh->shards.size(), blk = nqc * kc;
+    auto alloc = [](auto*& p, size_t count, const char* what) {
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(*p)), what);
+    };
+    for (size_t i = 0; i < S; ++i) {
+        DeviceGuard dg(sh->shards[i]->device);
+        alloc(sh->sq[i], nqc * sh->d, "cudaMalloc(shard queries)");
+        alloc(sh->sid[i], blk, "cudaMalloc(shard ids)");
+        alloc(sh->sdist[i], blk, "cudaMalloc(shard dists)");
+        alloc(sh->scnt[i], nqc, "cudaMalloc(shard counts)");
+    }
+    DeviceGuard dg(sh->shards[0]->device);
+    alloc(sh->gid, S * blk, "cudaMalloc(gather)");
+    alloc(sh->gdist, S * blk, "cudaMalloc(gather)");
+    alloc(sh->gcnt, S * nqc, "cudaMalloc(gather)");
+    alloc(sh->oid, blk, "cudaMalloc(merge)");
+    alloc(sh->odist, blk, "cudaMalloc(merge)");
+    alloc(sh->ocnt, nqc, "cudaMalloc(merge)");
+    sh->nq_cap = nqc;
+    sh->k_cap = kc;
+}
+
 // Device alias of a host buffer [p, p + bytes) when it lies in one mapped pinned
 // allocation (cudaHostAlloc / cudaMallocHost / registered-mapped memory, e.g. torch
 // pin_memory()); nullptr otherwise (pageable memory: the copy pipeline is used).
@@ -2075,9 +2152,31 @@ int tsdg_gpu_sharded_create_from_files(const char* const* tsdg_paths, const floa
                 return tsdg_gpu_index_create_from_file(tsdg_paths[i], bases[i], shard_n[i], d,
                                                        devices[i], &sh->shards[i]);
             });
+            // the per-shard top-k travel to the first shard's device: direct peer
+            // access over NVLink where the pair supports it (else the copy is staged)
+            const int m = devices[0];
+            for (uint32_t i = 1; i < nshards; ++i) {
+                const int dv = devices[i];
+                if (dv == m) continue;
+                int can = 0;
+                cuda_check(cudaDeviceCanAccessPeer(&can, m, dv), "cudaDeviceCanAccessPeer");
+                if (!can) continue;
+                DeviceGuard dg(m);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(dv, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else cuda_check(e, "cudaDeviceEnablePeerAccess");
+            }
+            sh->sq.assign(nshards, nullptr);
+            sh->sid.assign(nshards, nullptr);
+            sh->scnt.assign(nshards, nullptr);
+            sh->sdist.assign(nshards, nullptr);
+            sh->done.assign(nshards, nullptr);
+            for (uint32_t i = 0; i < nshards; ++i) {
+                DeviceGuard dg(devices[i]);
+                cuda_check(cudaEventCreateWithFlags(&sh->done[i], cudaEventDisableTiming), "event");
+            }
         } catch (...) {
-            for (auto* p : sh->shards)
-                if (p) tsdg_gpu_index_destroy(p);
+            sharded_free(sh.get());
             throw;
         }
         *out = sh.release();
@@ -2086,13 +2185,10 @@ int tsdg_gpu_sharded_create_from_files(const char* const* tsdg_paths, const floa
 
 int tsdg_gpu_sharded_destroy(tsdg_gpu_sharded* sh) {
     if (!sh) return TSDG_OK;
-    int rc = TSDG_OK;
-    for (auto* p : sh->shards) {
-        const int r = tsdg_gpu_index_destroy(p);
-        if (rc == TSDG_OK) rc = r;
-    }
-    delete sh;
-    return rc;
+    return guarded([&] {
+        sharded_free(sh);
+        delete sh;
+    });
 }
 
 int tsdg_gpu_sharded_search_bestfirst(tsdg_gpu_sharded* sh, const float* queries, uint32_t nq,
@@ -2104,71 +2200,61 @@ int tsdg_gpu_sharded_search_bestfirst(tsdg_gpu_sharded* sh, const float* queries
         if (!params) fail(TSDG_EINVAL, "bestfirst_search: null params");
         if (!queries || !ids) fail(TSDG_EINVAL, "bestfirst_search: null buffer");
         const uint32_t S = (uint32_t)sh->shards.size(), k = params->k, d = sh->d;
+        for (uint32_t i = 0; i < S; ++i) validate_bf(sh->shards[i], params);
         // every shard searches every query on its own device; the per-shard top-k
         // (local ids) are copied peer-to-peer (NVLink) into one [shard][query][k]
-        // block on the first shard's device and merged by (dist, global id) there
-        std::vector<uint32_t*> sid(S, nullptr), scnt(S, nullptr);
-        std::vector<float*> sdist(S, nullptr);
-        std::vector<cudaEvent_t> done(S, nullptr);
-        run_per_device(S, [&](size_t i) {
-            return guarded([&] {
-                tsdg_gpu_index* idx = sh->shards[i];
-                validate_bf(idx, params);
-                std::lock_guard<std::mutex> lk(idx->mu);
-                DeviceGuard dg(idx->device);
-                cudaStream_t st = idx->stream;
-                float* dq = dev_alloc<float>((size_t)nq * d, st);
-                sid[i] = dev_alloc<uint32_t>((size_t)nq * k, st);
-                sdist[i] = dev_alloc<float>((size_t)nq * k, st);
-                scnt[i] = dev_alloc<uint32_t>(nq, st);
-                cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * d * 4, cudaMemcpyHostToDevice, st),
-                           "H2D queries");
-                launch_bestfirst(idx, dq, nq, query_index_base, params, mode, sid[i], sdist[i], scnt[i],
-                                 nullptr, st);
-                cudaFreeAsync(dq, st);
-                cuda_check(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "event");
-                cuda_check(cudaEventRecord(done[i], st), "event record");
-            });
-        });
-        tsdg_gpu_index* m = sh->shards[0];
-        std::lock_guard<std::mutex> lk(m->mu);
-        DeviceGuard dg(m->device);
-        cudaStream_t st = m->stream;
+        // block on the first shard's device and merged by (dist, global id) there.
+        // The workspace persists across calls; a failed shard leaves nothing behind.
+        std::lock_guard<std::mutex> slk(sh->mu);
+        sharded_reserve(sh, nq, k);
         const size_t blk = (size_t)nq * k;
-        uint32_t* gid = dev_alloc<uint32_t>(S * blk, st);
-        float* gdist = dev_alloc<float>(S * blk, st);
-        uint32_t* gcnt = dev_alloc<uint32_t>((size_t)S * nq, st);
-        for (uint32_t i = 0; i < S; ++i) {
-            const int dev = sh->shards[i]->device;
-            cuda_check(cudaStreamWaitEvent(st, done[i], 0), "wait shard");
-            cuda_check(cudaMemcpyPeerAsync(gid + i * blk, m->device, sid[i], dev, blk * 4, st), "peer ids");
-            cuda_check(cudaMemcpyPeerAsync(gdist + i * blk, m->device, sdist[i], dev, blk * 4, st), "peer dists");
-            cuda_check(cudaMemcpyPeerAsync(gcnt + (size_t)i * nq, m->device, scnt[i], dev, (size_t)nq * 4, st),
-                       "peer counts");
+        try {
+            run_per_device(S, [&](size_t i) {
+                return guarded([&] {
+                    tsdg_gpu_index* idx = sh->shards[i];
+                    std::lock_guard<std::mutex> lk(idx->mu);
+                    DeviceGuard dg(idx->device);
+                    cudaStream_t st = idx->stream;
+                    float* dq = sh->sq[i];
+                    cuda_check(cudaMemcpyAsync(dq, queries, (size_t)nq * d * 4, cudaMemcpyHostToDevice, st),
+                               "H2D queries");  // rows of d floats (the kernels' query stride)
+                    launch_bestfirst(idx, dq, nq, query_index_base, params, mode, sh->sid[i], sh->sdist[i],
+                                     sh->scnt[i], nullptr, st);
+                    cuda_check(cudaEventRecord(sh->done[i], st), "event record");
+                });
+            });
+            tsdg_gpu_index* m = sh->shards[0];
+            std::lock_guard<std::mutex> lk(m->mu);
+            DeviceGuard dg(m->device);
+            cudaStream_t st = m->stream;
+            for (uint32_t i = 0; i < S; ++i) {
+                const int dev = sh->shards[i]->device;
+                cuda_check(cudaStreamWaitEvent(st, sh->done[i], 0), "wait shard");
+                cuda_check(cudaMemcpyPeerAsync(sh->gid + i * blk, m->device, sh->sid[i], dev, blk * 4, st),
+                           "peer ids");
+                cuda_check(cudaMemcpyPeerAsync(sh->gdist + i * blk, m->device, sh->sdist[i], dev, blk * 4, st),
+                           "peer dists");
+                cuda_check(cudaMemcpyPeerAsync(sh->gcnt + (size_t)i * nq, m->device, sh->scnt[i], dev,
+                                               (size_t)nq * 4, st),
+                           "peer counts");
+            }
+            const int rc = tsdg_gpu_merge_shards_device(sh->gid, sh->gdist, sh->gcnt, sh->offsets.data(), S,
+                                                        nq, k, sh->oid, sh->odist, sh->ocnt, st);
+            if (rc != TSDG_OK) fail(rc, tsdg_gpu_last_error());
+            cuda_check(cudaMemcpyAsync(ids, sh->oid, blk * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+            if (dists)
+                cuda_check(cudaMemcpyAsync(dists, sh->odist, blk * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+            if (counts)
+                cuda_check(cudaMemcpyAsync(counts, sh->ocnt, (size_t)nq * 4, cudaMemcpyDeviceToHost, st),
+                           "D2H counts");
+            cuda_check(cudaStreamSynchronize(st), "sharded search");
+        } catch (...) {
+            for (auto* idx : sh->shards) {  // no shard work left in flight on the workspace
+                DeviceGuard dg(idx->device);
+                cudaStreamSynchronize(idx->stream);
+            }
+            throw;
         }
-        uint32_t* oid = dev_alloc<uint32_t>(blk, st);
-        float* odist = dev_alloc<float>(blk, st);
-        uint32_t* ocnt = dev_alloc<uint32_t>(nq, st);
-        const int rc = tsdg_gpu_merge_shards_device(gid, gdist, gcnt, sh->offsets.data(), S, nq, k, oid,
-                                                    odist, ocnt, st);
-        if (rc != TSDG_OK) fail(rc, tsdg_gpu_last_error());
-        cuda_check(cudaMemcpyAsync(ids, oid, blk * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
-        if (dists) cuda_check(cudaMemcpyAsync(dists, odist, blk * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
-        if (counts) cuda_check(cudaMemcpyAsync(counts, ocnt, (size_t)nq * 4, cudaMemcpyDeviceToHost, st), "D2H counts");
-        cuda_check(cudaStreamSynchronize(st), "sharded search");
-        for (uint32_t i = 0; i < S; ++i) {
-            DeviceGuard di(sh->shards[i]->device);
-            cudaFree(sid[i]);
-            cudaFree(sdist[i]);
-            cudaFree(scnt[i]);
-            cudaEventDestroy(done[i]);
-        }
-        cudaFreeAsync(gid, st);
-        cudaFreeAsync(gdist, st);
-        cudaFreeAsync(gcnt, st);
-        cudaFreeAsync(oid, st);
-        cudaFreeAsync(odist, st);
-        cudaFreeAsync(ocnt, st);
     });
 }
 
