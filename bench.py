@@ -379,6 +379,25 @@ def c4_section(args, dev):
                         "TSDG from the reference builder (nn_descent k=64)", **best}
 
 
+def gpu_local_cpus(device: int):
+    """Host CPUs attached to `device` (NVML CPU affinity), or None.  The host-pointer
+    (zero-copy) path streams queries and results between pinned host memory and the
+    GPU while the kernel runs, so the pinned buffers belong on the GPU's own NUMA node:
+    the process runs on those CPUs while it allocates and times them (the CPU baseline
+    gets every core back)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        avail = os.sched_getaffinity(0)
+        cpus &= avail
+        return cpus if cpus and cpus != avail else None
+    except Exception:
+        return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -562,6 +581,12 @@ def main():
     from paper_2204_00824_b200 import _native
     from paper_2204_00824_b200.search import BestFirstParams, GpuIndex, load_tsdg
 
+    all_cpus = os.sched_getaffinity(0)
+    local_cpus = gpu_local_cpus(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
+                                if os.environ.get("CUDA_VISIBLE_DEVICES", "").replace(",", "").isdigit()
+                                else local)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -683,6 +708,9 @@ def main():
     e2e_val = total_q * args.steps / e2e_s
     assert np.array_equal(h_ids.numpy().view(np.uint32), head["ids"]), "e2e result differs"
 
+    if local_cpus:  # the reference (CPU baseline, small-batch reference) gets every core
+        os.sched_setaffinity(0, all_cpus)
+
     # ---- secondary workloads (not the headline): small batch, sharded base, C4 -----
     extras = {}
     if not args.no_extras:
@@ -748,6 +776,7 @@ def main():
             "e2e": {"value": e2e_val, "unit": "queries/s",
                     "h2d_bytes_per_step": int(queries.nbytes),
                     "d2h_bytes_per_step": int(nq * k * 8 + nq * 4),
+                    "host_cpus": f"{len(local_cpus)} GPU-local CPUs (NVML affinity)" if local_cpus else "all",
                     "transfer": "zero-copy (kernel reads/writes pinned host memory)"
                     if os.environ.get("TSDG_ZERO_COPY", "1") != "0" else "copy pipeline (2 chunks, 2 streams)"},
             "gpu_launches": head["launches"],

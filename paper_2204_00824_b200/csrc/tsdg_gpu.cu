@@ -1608,6 +1608,11 @@ int tsdg_gpu_search_bestfirst(tsdg_gpu_index* idx, const float* queries, uint32_
             float* zd = mapped_alias(dists, (size_t)nq * k * 4);
             uint32_t* zc = mapped_alias(counts, (size_t)nq * 4);
             tsdg_query_stats* zs = mapped_alias(stats, (size_t)nq * sizeof(tsdg_query_stats));
+            if (env_int("TSDG_DEBUG_PATH", 0))
+                std::fprintf(stderr, "[tsdg] bestfirst host call: q=%p i=%p d=%p c=%p s=%p -> %s\n",
+                             (const void*)zq, (void*)zi, (void*)zd, (void*)zc, (void*)zs,
+                             (zq && zi && (zd || !dists) && (zc || !counts) && (zs || !stats))
+                                 ? "zero-copy" : "copy pipeline");
             if (zq && zi && (zd || !dists) && (zc || !counts) && (zs || !stats)) {
                 launch_bestfirst(idx, zq, nq, query_index_base, params, mode, zi, zd, zc, zs,
                                  idx->stream);
