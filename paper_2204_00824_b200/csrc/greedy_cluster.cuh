@@ -49,6 +49,8 @@ struct GcArgs {
     uint32_t* walk_hops;
     uint32_t* walk_evals;
     int cluster;         // 1: the t0 CTAs of a query form one cluster
+    uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
+                            // evaluated node (the next hop's u is one of them)
     uint32_t npow2;      // pool size for the in-cluster merge
     uint32_t dch, slots;
     uint32_t off_query, off_stage, off_part, off_bar, off_ctl, off_list, off_pool, off_rowid;
@@ -112,6 +114,17 @@ __device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_r
     return m;
 }
 
+// The next hop expands one of the nodes evaluated in this hop (the closest of
+// R_temp), so their deg_cut entries and adjacency heads are pulled into L2 as soon as
+// their ids are known: the next hop's adjacency read then hits L2 instead of DRAM.
+__device__ __forceinline__ void gc_prefetch_adj(const GcArgs& a, bool valid, uint32_t e) {
+    if (!a.adj_prefetch || !valid) return;
+    const uint32_t* row = a.adj + (size_t)e * a.R;
+    prefetch_l2(row);
+    if (a.R > 32) prefetch_l2(row + 32);
+    prefetch_l2(a.degcut + e);
+}
+
 // One walk (CTA) of query q: select_start + hops + (cluster mode) the in-cluster merge
 // of the t0 walks into `o`.  gq: the query (any memory space the SM can read: device
 // memory, or mapped host memory); s: the walk's RNG stream index.
@@ -138,6 +151,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     if (warp == 0) {
         const uint64_t st = a.walk_states ? a.walk_states[walk] : fork_state(a.seed, s);
         const uint32_t v = draw_below(st, (uint32_t)lane, a.n);
+        gc_prefetch_adj(a, true, v);
         float sd = gather_eval<METRIC, FAST, STAGE>(w, g, true, v, lane);
         uint32_t si = v;
         warp_argmin(sd, si);
@@ -166,6 +180,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         pend = j0 < deg;
         e0 = pend ? __ldg(a.adj + (size_t)u * a.R + j0) : kInvalid;
         gather_issue(w, g, pend, e0, lane);
+        gc_prefetch_adj(a, pend, e0);
     }
     TR_MARK(2)
     PH_DECL
@@ -196,6 +211,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             const uint32_t j = gi * 32 + lane;
             const bool valid = j < deg;
             const uint32_t e = valid ? (gi == (uint32_t)warp ? e0 : __ldg(arow + j)) : kInvalid;
+            gc_prefetch_adj(a, valid, e);
             const float dist = gather_eval<METRIC, FAST, STAGE>(w, g, valid, e, lane);
             if (valid && dist < md) {
                 md = dist;
@@ -258,6 +274,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             pend = j0 < ndeg;
             e0 = pend ? ne : kInvalid;
             gather_issue(w, g, pend, e0, lane);
+            gc_prefetch_adj(a, pend, e0);
         }
         PH_MARK(3)  // warp 0: combine + merge_halves
         __syncthreads();

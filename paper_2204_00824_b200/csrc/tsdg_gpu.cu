@@ -566,6 +566,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.vec = idx->vec;
     a.adj = idx->adj;
     a.degcut = get_degcut(idx, p->lambda_cut, st);
+    a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 1);
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
