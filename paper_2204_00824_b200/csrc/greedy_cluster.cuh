@@ -115,8 +115,10 @@ __device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_r
 }
 
 // The next hop expands one of the nodes evaluated in this hop (the closest of
-// R_temp), so their deg_cut entries and adjacency heads are pulled into L2 as soon as
-// their ids are known: the next hop's adjacency read then hits L2 instead of DRAM.
+// R_temp), so their deg_cut entries and adjacency heads can be pulled into L2 as soon
+// as their ids are known.  Off by default (TSDG_GC_ADJ_PREFETCH=1): on C2 it moved
+// batch-1/8/64 latency by < 1% — the next hop's adjacency load already overlaps the
+// warp-0 merge, so it is not on the critical path.
 __device__ __forceinline__ void gc_prefetch_adj(const GcArgs& a, bool valid, uint32_t e) {
     if (!a.adj_prefetch || !valid) return;
     const uint32_t* row = a.adj + (size_t)e * a.R;

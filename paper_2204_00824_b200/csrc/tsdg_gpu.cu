@@ -439,9 +439,14 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     a.slots = (uint32_t)std::max(1, std::min(32, env_int("TSDG_SLOTS", 16)));
     a.prefetch = (uint32_t)env_int("TSDG_PREFETCH", 0);
     a.batch_min = (uint32_t)std::max(0, env_int("TSDG_BATCH_MIN", 0));
-    // fast mode, k <= 31: register-direct warp-cooperative kernel (bf_fast.cuh);
-    // TSDG_FAST_KERNEL=staged keeps the staged kernel for comparison
-    if (mode == TSDG_MODE_FAST && a.k <= 31 && !env_is("TSDG_FAST_KERNEL", "staged")) {
+    // fast mode, k <= 31, rows of at most 128 floats: register-direct warp-cooperative
+    // kernel (bf_fast.cuh).  Wider rows keep the staged kernel: at d = 960 (C4) the
+    // register-direct form measured 24.0 ms vs 15.9 ms for the staged deterministic
+    // kernel (its query no longer fits in registers and a row takes 8 batch rounds).
+    // TSDG_FAST_KERNEL=staged / =register forces either.
+    const bool reg_fast = env_is("TSDG_FAST_KERNEL", "register") ||
+                          (idx->ld <= 128 && !env_is("TSDG_FAST_KERNEL", "staged"));
+    if (mode == TSDG_MODE_FAST && a.k <= 31 && reg_fast) {
         // bit 0: bulk L2 prefetch of the rows past a hop's first batch (default, C2:
         // 0.85 -> 0.79 ms); bit 1: L2 prefetch of admitted nodes' adjacency (slower)
         a.prefetch = (uint32_t)env_int("TSDG_FAST_PREFETCH", 1);
@@ -566,7 +571,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.vec = idx->vec;
     a.adj = idx->adj;
     a.degcut = get_degcut(idx, p->lambda_cut, st);
-    a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 1);
+    a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 0);  // measured: no gain (C2 batch 1/8/64)
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
