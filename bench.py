@@ -371,12 +371,14 @@ def c4_section(args, dev):
         ms = float(np.median(times))
         best = {"k_search": k, "recall_at_10": rec, "value": nq / ms * 1e3, "unit": "queries/s",
                 "ms_per_batch": ms, "roofline_achieved_GBps": alg / ms / 1e6,
-                "roofline_frac": alg / ms / 1e6 / peaks()[0]}
+                "roofline_frac": alg / ms / 1e6 / peaks()[0], "alg_bytes_per_launch": int(alg)}
         if rec >= 0.95:
             break
     idx.close()
+    traffic = profiled_traffic("c4_fast") if args.mode == "fast" else None
     return {"workload": "GIST1M-shaped 1M x 960 fp32 L2 low-LID (latent 26), batch 10K, "
-                        "TSDG from the reference builder (nn_descent k=64)", **best}
+                        "TSDG from the reference builder (nn_descent k=64)", **best,
+            "traffic": traffic, "traffic_capture": "profiles/r2_bf_staged_c4.md (k_search=24)"}
 
 
 def gpu_local_cpus(device: int):
