@@ -49,6 +49,8 @@ struct GcArgs {
     uint32_t* walk_hops;
     uint32_t* walk_evals;
     int cluster;         // 1: the t0 CTAs of a query form one cluster
+    uint32_t merge_warp;    // 1: warp 0 only combines / merges, warps 1.. evaluate the
+                            // hop's groups (its merge then overlaps their gathers)
     uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
                             // evaluated node (the next hop's u is one of them)
     uint32_t npow2;      // pool size for the in-cluster merge
@@ -172,8 +174,14 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     // Pipelined hops (TMA staging, whole rows in one round): each warp's first group
     // of the next hop is issued as soon as the next node is known — while warp 0 runs
     // merge_halves — and completed at the top of the next hop.
-    const bool pipe = STAGE == kStageTma && a.ld <= a.dch && a.slots >= 32;
-    const uint32_t j0 = (uint32_t)warp * 32 + lane;
+    const bool pipe = a.ld <= a.dch && a.slots >= 32;  // TMA or LDGSTS split gathers
+    // evaluating warps: all, or warps 1.. when warp 0 is kept for combine + merge (then
+    // the next hop's first groups are issued by warps 1.. while warp 0 merges, and the
+    // merge leaves the hop's critical path)
+    const uint32_t ew0 = a.merge_warp ? 1u : 0u, nev = (uint32_t)kGcWarps - ew0;
+    const bool evaluates = (uint32_t)warp >= ew0;
+    const uint32_t ew = evaluates ? (uint32_t)warp - ew0 : 0u;  // this warp's first group
+    const uint32_t j0 = evaluates ? ew * 32 + lane : 0xFFFFFFFFu;
     uint32_t deg = 0, e0 = kInvalid;
     bool pend = false;  // this lane's row of the pre-issued group
     if (pipe) {
@@ -181,7 +189,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         deg = __ldg(a.degcut + u);
         pend = j0 < deg;
         e0 = pend ? __ldg(a.adj + (size_t)u * a.R + j0) : kInvalid;
-        gather_issue(w, g, pend, e0, lane);
+        gather_issue_s<STAGE>(w, g, pend, e0, lane);
         gc_prefetch_adj(a, pend, e0);
     }
     TR_MARK(2)
@@ -201,18 +209,18 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         float md = kInf;
         uint32_t mi = kInvalid, mg = 0xFFFFFFFFu;
         if (pipe) {  // the first group was issued during the previous hop's merge
-            const float dist = gather_complete<METRIC, FAST>(w, g, pend, lane);
+            const float dist = gather_complete<METRIC, FAST, STAGE>(w, g, pend, lane);
             if (pend && dist < md) {
                 md = dist;
                 mi = e0;
-                mg = warp;
+                mg = ew;
             }
             pend = false;
         }
-        for (uint32_t gi = pipe ? warp + kGcWarps : warp; gi < ngroups; gi += kGcWarps) {
+        for (uint32_t gi = pipe ? ew + nev : ew; evaluates && gi < ngroups; gi += nev) {
             const uint32_t j = gi * 32 + lane;
             const bool valid = j < deg;
-            const uint32_t e = valid ? (gi == (uint32_t)warp ? e0 : __ldg(arow + j)) : kInvalid;
+            const uint32_t e = valid ? (gi == ew ? e0 : __ldg(arow + j)) : kInvalid;
             gc_prefetch_adj(a, valid, e);
             const float dist = gather_eval<METRIC, FAST, STAGE>(w, g, valid, e, lane);
             if (valid && dist < md) {
@@ -275,16 +283,19 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             deg = ndeg;
             pend = j0 < ndeg;
             e0 = pend ? ne : kInvalid;
-            gather_issue(w, g, pend, e0, lane);
+            if (e0 == 0xFFFFFFFEu) asm volatile("" ::: "memory");  // (phases build: e0 loaded)
+            PH_MARK(3)  // combine + (warp 0) merge_halves / (others) next adjacency
+            gather_issue_s<STAGE>(w, g, pend, e0, lane);
             gc_prefetch_adj(a, pend, e0);
+            PH_MARK(5)  // next hop's row copies issued
+        } else {
+            PH_MARK(3)
         }
-        PH_MARK(3)  // warp 0: combine + merge_halves
         __syncthreads();
         TR_MARK(3 + t)
         PH_MARK(4)  // barrier
     }
-    if (pipe) gather_complete<METRIC, FAST>(w, g, pend, lane);  // drain a pre-issued group
-    PH_MARK(5)
+    if (pipe) gather_complete<METRIC, FAST, STAGE>(w, g, pend, lane);  // drain a pre-issued group
 
     if (!a.cluster) {
         if (warp == 0) {

@@ -274,7 +274,36 @@ __device__ __forceinline__ void gather_issue(WarpStage& w, const Geom& g, bool n
     if (need) bulk_g2s(w.stage + rank * pitch, g.vec + (size_t)e * g.ld, g.ld * 4u, w.bar);
 }
 
-template <int METRIC, bool FAST>
+// LDGSTS form of gather_issue (rows of at most 128 floats, w.rowid set): the needed
+// lanes publish their row ids by rank, then every lane copies 16-byte pieces with
+// cp.async (one coalesced row per warp instruction at d = 128) — no per-row TMA
+// request, which the greedy hop found issue-bound (~30 cycles per 512-B row).
+__device__ __forceinline__ void gather_issue_ldgsts(WarpStage& w, const Geom& g, bool need,
+                                                    uint32_t e, int lane) {
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return;
+    const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
+    const uint32_t cnt = __popc(nm);
+    __syncwarp();  // the slots' previous rows have been consumed
+    if (need) w.rowid[__popc(nm & ((1u << lane) - 1u))] = e;
+    __syncwarp();
+    const uint32_t nvec = g.ld >> 2, rpi = 32u / nvec;
+    const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
+    for (uint32_t t = 0; t < cnt; t += rpi) {
+        const uint32_t row = t + sub;
+        if (sub < rpi && row < cnt)
+            cp_async16(w.stage + row * pitch + piece * 4, g.vec + (size_t)w.rowid[row] * g.ld + piece * 4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int STAGE>
+__device__ __forceinline__ void gather_issue_s(WarpStage& w, const Geom& g, bool need, uint32_t e,
+                                               int lane) {
+    if (STAGE == kStageTma) gather_issue(w, g, need, e, lane);
+    else gather_issue_ldgsts(w, g, need, e, lane);
+}
+
+template <int METRIC, bool FAST, int STAGE = kStageTma>
 __device__ __forceinline__ float gather_complete(WarpStage& w, const Geom& g, bool need, int lane) {
     const float kInf = __int_as_float(0x7f800000);
     const unsigned nm = __ballot_sync(kFull, need);
@@ -282,8 +311,13 @@ __device__ __forceinline__ float gather_complete(WarpStage& w, const Geom& g, bo
     const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
     const uint32_t cnt = __popc(nm);
     const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
-    mbar_wait(w.bar, w.parity);
-    w.parity ^= 1u;
+    if (STAGE == kStageTma) {
+        mbar_wait(w.bar, w.parity);
+        w.parity ^= 1u;
+    } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
     float dist = kInf;
     if ((uint32_t)lane < cnt) {  // lane r reduces slot r, in the reference's order
         const float* srow = w.stage + lane * pitch;

@@ -572,6 +572,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.adj = idx->adj;
     a.degcut = get_degcut(idx, p->lambda_cut, st);
     a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 0);  // measured: no gain (C2 batch 1/8/64)
+    a.merge_warp = (uint32_t)env_int("TSDG_GC_MERGE_WARP", 1);
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
@@ -618,9 +619,10 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
     }
     using GcKernel = void (*)(GcArgs);
     GcKernel kern;
-    // row staging: LDGSTS (one coalesced 512 B row per warp instruction) or TMA bulk
-    // copies (issued lane by lane through an ELECT loop); TSDG_GC_STAGE selects
-    const bool ldg = env_is("TSDG_GC_STAGE", "ldgsts");  // measured: TMA 83 us, LDGSTS 92 us
+    // row staging: TMA bulk copies (one per row) or LDGSTS (one coalesced 512 B row per
+    // warp instruction); TSDG_GC_STAGE selects.  Both pipelined across hops; C2 batch 1,
+    // t0=10: TMA 51 us, LDGSTS 59 us (its 32 cp.async per lane issue slower)
+    const bool ldg = env_is("TSDG_GC_STAGE", "ldgsts");
     if (idx->metric == 0)
         kern = fast ? (ldg ? greedy_cta_kernel<0, true, kStageLdgsts> : greedy_cta_kernel<0, true, kStageTma>)
                     : (ldg ? greedy_cta_kernel<0, false, kStageLdgsts> : greedy_cta_kernel<0, false, kStageTma>);

@@ -30,7 +30,8 @@ torch.cuda.synchronize()
 lib.tsdg_gpu_phase_read(out.ctypes.data, 1)
 hops = int(st.cpu().numpy()[:, 0].sum())  # summed over walks
 warps = nq * t0 * 4
-names = ["start", "gather+dist", "barrier1", "merge(w0)", "barrier2", "-", "cluster wait", "pool merge"]
+names = ["start", "gather+dist", "barrier1", "combine+merge(w0)/next adjacency", "barrier2",
+         "row copy issue", "cluster wait", "pool merge"]
 print(json.dumps({"t0": t0, "walk_hops": hops / (nq * t0),
                   "cycles_per_walk_warp": {names[i]: round(float(out[i]) / warps) for i in range(8)},
-                  "per_hop": {names[i]: round(float(out[i]) / (hops * 4)) for i in (1, 2, 3, 4)}}))
+                  "per_hop": {names[i]: round(float(out[i]) / (hops * 4)) for i in (1, 2, 3, 5, 4)}}))
