@@ -6,32 +6,33 @@
 namespace tsdg_dev {
 
 template <int METRIC, int SEG>
-static BfFastKernel pick(int variant) {
+static BfFastKernel pick(int variant, bool pair) {
+    if (pair) return bf_fast_kernel<METRIC, 8, SEG, 12, false, true>;
     if (METRIC == 0 && SEG == 1) {
         switch (variant) {
-            case 1: return bf_fast_kernel<METRIC, 8, SEG, 16, false>;
-            case 2: return bf_fast_kernel<METRIC, 16, SEG, 12, false>;
-            case 3: return bf_fast_kernel<METRIC, 16, SEG, 10, false>;
-            case 4: return bf_fast_kernel<METRIC, 8, SEG, 12, true>;
-            case 5: return bf_fast_kernel<METRIC, 8, SEG, 10, true>;
-            case 6: return bf_fast_kernel<METRIC, 4, SEG, 16, false>;
-            case 7: return bf_fast_kernel<METRIC, 4, SEG, 12, false>;
+            case 1: return bf_fast_kernel<METRIC, 8, SEG, 16, false, false>;
+            case 2: return bf_fast_kernel<METRIC, 16, SEG, 12, false, false>;
+            case 3: return bf_fast_kernel<METRIC, 16, SEG, 10, false, false>;
+            case 4: return bf_fast_kernel<METRIC, 8, SEG, 12, true, false>;
+            case 5: return bf_fast_kernel<METRIC, 8, SEG, 10, true, false>;
+            case 6: return bf_fast_kernel<METRIC, 4, SEG, 16, false, false>;
+            case 7: return bf_fast_kernel<METRIC, 4, SEG, 12, false, false>;
             default: break;
         }
     }
-    return bf_fast_kernel<METRIC, 8, SEG, 12, false>;
+    return bf_fast_kernel<METRIC, 8, SEG, 12, false, false>;
 }
 template <int METRIC>
-static BfFastKernel pick(int seg, int variant) {
-    if (seg == 1) return pick<METRIC, 1>(variant);
-    if (seg == 2) return pick<METRIC, 2>(variant);
-    return pick<METRIC, 0>(variant);
+static BfFastKernel pick(int seg, int variant, bool pair) {
+    if (seg == 1) return pick<METRIC, 1>(variant, pair);
+    if (seg == 2) return pick<METRIC, 2>(variant, pair);
+    return pick<METRIC, 0>(variant, pair);
 }
 
-BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant) {
-    if (metric == 0) return pick<0>(seg, variant);
-    if (metric == 1) return pick<1>(seg, variant);
-    return pick<2>(seg, variant);
+BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant, bool pair) {
+    if (metric == 0) return pick<0>(seg, variant, pair);
+    if (metric == 1) return pick<1>(seg, variant, pair);
+    return pick<2>(seg, variant, pair);
 }
 
 }  // namespace tsdg_dev

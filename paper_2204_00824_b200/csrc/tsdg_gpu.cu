@@ -455,13 +455,24 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         const bool reg_q = idx->ld <= 128 && idx->ld == idx->d &&
                            (reinterpret_cast<uintptr_t>(d_queries) & 15u) == 0;
         const int seg = reg_q ? (idx->ld == 128 ? 1 : 2) : 0;
-        const BfKernel kern =
-            bf_fast_kernel_for(idx->metric, seg, env_int("TSDG_FAST_VARIANT", 0));
-        const size_t smem = (size_t)a.warp_smem * kFastWarps;
-        set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast)");
-        const int grid = grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, kFastWarps);
+        // Paired form (two warps per query) when the batch leaves most resident query
+        // slots empty: fewer queries than one CTA per slot of the one-warp-per-query
+        // launch (a strong-scaled rank's slice).  TSDG_FAST_PAIR=0 / 1 forces.
+        const BfKernel single = bf_fast_kernel_for(idx->metric, seg, env_int("TSDG_FAST_VARIANT", 0));
+        const size_t smem1 = (size_t)a.warp_smem * kFastWarps;
+        set_smem(reinterpret_cast<const void*>(single), smem1, "cudaFuncSetAttribute(bf_fast)");
+        const int slots = grid_for(single, kFastWarps * 32, smem1, idx->sm_count, 0xFFFFFFFFu, 1);
+        const int pair_env = env_int("TSDG_FAST_PAIR", -1);
+        const bool pair = pair_env >= 0 ? pair_env == 1 : nq <= (uint32_t)slots;
+        const BfKernel kern = pair ? bf_fast_kernel_for(idx->metric, seg, 0, true) : single;
+        const size_t smem = pair ? (size_t)a.warp_smem + 16 : smem1;
+        if (pair) set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast pair)");
+        // work fetches: one per query plus one final per fetching warp (the leader only
+        // in the paired form)
+        const int grid = pair ? grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, 1)
+                              : grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, kFastWarps);
         kern<<<grid, kFastWarps * 32, smem, st>>>(a);
-        commit_counter(idx, tk, nq, (uint64_t)grid * kFastWarps, st);
+        commit_counter(idx, tk, nq, (uint64_t)grid * (pair ? 1 : kFastWarps), st);
         g_launches++;
         cuda_check(cudaGetLastError(), "bf_fast_kernel launch");
         return;
