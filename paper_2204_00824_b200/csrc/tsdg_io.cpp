@@ -99,7 +99,15 @@ int parse_header(Reader& r, tsdg_graph_header& h) {
         r.err = r.path + ": unsupported TSDG version " + std::to_string(version);
         return TSDG_ERUNTIME;
     }
-    h.n = static_cast<uint32_t>(r.le<uint64_t>());
+    // diversify.cpp:286 narrows the u64 count to the u32 NodeId range silently; a
+    // count past that range cannot describe a valid graph (ids are u32), so it is
+    // reported instead of truncated
+    const uint64_t n64 = r.le<uint64_t>();
+    if (r.ok && n64 > 0xFFFFFFFFull) {
+        r.err = r.path + ": node count " + std::to_string(n64) + " exceeds the 32-bit id range";
+        return TSDG_ERUNTIME;
+    }
+    h.n = static_cast<uint32_t>(n64);
     h.metric = r.le<uint8_t>();
     h.k = r.le<uint32_t>();
     const uint32_t abits = r.le<uint32_t>();

@@ -199,3 +199,14 @@ def test_index_from_files_errors(tmp_path, fixtures):
     with pytest.raises(Exception) as e_dev:
         GpuIndex.from_files(str(cut), str(p))
     assert str(e_dev.value) == str(e_host.value) and "truncated" in str(e_dev.value)
+
+
+def test_tsdg_node_count_beyond_u32_is_an_error(tmp_path):
+    """A .tsdg header whose u64 node count exceeds the u32 id range is reported, not
+    narrowed (diversify.cpp:286 narrows it silently)."""
+    from paper_2204_00824_b200.search import InvalidArgument, TsdgRuntimeError, load_tsdg
+    p = tmp_path / "big.tsdg"
+    with open(p, "wb") as f:
+        f.write(b"TSDG" + struct.pack("<IQBIfH", 1, (1 << 32) + 5, 0, 8, 1.2, 9))
+    with pytest.raises((TsdgRuntimeError, InvalidArgument), match="32-bit id range"):
+        load_tsdg(str(p))
