@@ -685,7 +685,12 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
 bool use_cta_greedy(const tsdg_gpu_index* idx, uint32_t nq, uint32_t t0) {
     if (env_is("TSDG_GREEDY", "cta")) return true;
     if (env_is("TSDG_GREEDY", "warp")) return false;
-    return (uint64_t)nq * t0 <= 2ull * idx->sm_count;  // measured crossover, C2 (profiles/)
+    // measured crossover on C2 (profiles/greedy_crossover_r2.jsonl): the cluster kernel
+    // is faster up to ~4.5 walks per SM (t0=10: 64 queries 94 vs 125 us; 128 queries
+    // 158 vs 132 us; t0=16: 32 queries 94 vs 122 us, 64 queries 155 vs 130 us)
+    const int mx = env_int("TSDG_GREEDY_CTA_MAX_WALKS", 0);
+    const uint64_t limit = mx > 0 ? (uint64_t)mx : (uint64_t)idx->sm_count * 9 / 2;
+    return (uint64_t)nq * t0 <= limit;
 }
 
 void launch_greedy(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,

@@ -67,8 +67,8 @@ os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 with open(os.path.join(ROOT, "profiles", f"{tag}.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
 # traffic.json
-mode = None
-if "bf_kernel<" in kname:
+mode = os.environ.get("TRAFFIC_KEY")  # e.g. c4_fast; default: parsed for the C2 captures
+if mode is None and "bf_kernel<" in kname:
     fast = kname.split("bf_kernel<")[1].split(",")[1].strip()
     mode = "fast" if fast in ("1", "true") else "det"
 if mode:
