@@ -344,7 +344,11 @@ __device__ __forceinline__ void row_prefetch(const BfArgs& a, bool want, uint32_
 // evaluation of more than B rows the helper warp takes the rows past the leader's
 // share.  ctl (shared memory): [0] command (1 evaluate, 0 exit), [1] rows, [2] the
 // leader's share (a multiple of B), [3] the current query.  One evaluation = one
-// "go" and one "done" CTA barrier on both warps.
+// "go" and one "done" barrier on both warps — the non-.aligned named barrier 1 (the
+// two warps reach it from different code), never __syncthreads().
+__device__ __forceinline__ void pair_barrier() {
+    asm volatile("barrier.sync 1, 64;" ::: "memory");
+}
 template <int METRIC, int B, int SEG, bool PIPE, bool PAIR>
 __device__ __forceinline__ void coop_eval(const FastGeom& g, const uint32_t* lst, float* dl,
                                           uint32_t cnt, ulonglong2 q, int lane,
@@ -359,9 +363,9 @@ __device__ __forceinline__ void coop_eval(const FastGeom& g, const uint32_t* lst
         ctl[1] = cnt;
         ctl[2] = h;
     }
-    __syncthreads();  // go
+    pair_barrier();  // go
     eval_list<METRIC, B, SEG, PIPE>(g, lst, dl, h, q, lane);
-    __syncthreads();  // done: the helper's dl entries are visible
+    pair_barrier();  // done: the helper's dl entries are visible
 }
 
 // Admission replay of one 32-edge chunk in edge order (bestfirst_search.cpp:85-96).
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
         uint32_t cur = kInvalid;
         ulonglong2 q = make_ulonglong2(0ull, 0ull);
         for (;;) {
-            __syncthreads();  // go
+            pair_barrier();  // go
             if (ctl[0] == 0u) break;
             const uint32_t qi = ctl[3], cnt = ctl[1], h = ctl[2];
             if (SEG != 0 && qi != cur) {
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
                                            : make_ulonglong2(0ull, 0ull);
             }
             eval_list<METRIC, B, SEG, PIPE>(g, lst + h, dl + h, cnt - h, q, lane);
-            __syncthreads();  // done
+            pair_barrier();  // done
         }
         return;
     }
@@ -608,7 +612,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
     }
     if (PAIR) {  // release the helper
         if (lane == 0) ctl[0] = 0u;
-        __syncthreads();
+        pair_barrier();
     }
 }
 
