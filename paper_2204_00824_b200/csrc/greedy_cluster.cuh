@@ -50,19 +50,13 @@ struct GcArgs {
     uint32_t* walk_evals;
     int cluster;         // 1: the t0 CTAs of a query form one cluster
     uint32_t merge_warp;    // 1: warp 0 only combines / merges, warps 1.. evaluate the
-                            // hop's groups (its merge then overlaps their gathers)
+                            // hop's edges (its merge then overlaps their gathers)
+    uint32_t slice;         // edges per evaluating warp per round (16 or 32)
     uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
                             // evaluated node (the next hop's u is one of them)
     uint32_t npow2;      // pool size for the in-cluster merge
     uint32_t dch, slots;
-    uint32_t off_query, off_stage, off_part, off_bar, off_ctl, off_list, off_pool, off_rowid;
-};
-
-struct GcPart {
-    float d;
-    uint32_t id;
-    uint32_t group;
-    uint32_t pad;
+    uint32_t off_query, off_stage, off_bar, off_ctl, off_list, off_pool, off_rowid, off_pos;
 };
 
 struct GcCtl {
@@ -92,7 +86,6 @@ struct GcOut {
 // Shared-memory views of one CTA (carved by the host, GcArgs::off_*).
 struct GcSmem {
     float* sq;
-    GcPart* part;
     GcCtl* ctl;
     float* list_d;
     uint32_t* list_i;
@@ -100,12 +93,15 @@ struct GcSmem {
     uint32_t* pool_i;
     uint32_t* scan;
     uint32_t* walk_cnt;  // rank 0: 2 x t0 (hops, evals) pushed by the walks
+    float* pos_d;        // this hop's distance / id by adjacency position (R entries)
+    uint32_t* pos_i;
 };
 
 __device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_raw) {
     GcSmem m;
     m.sq = reinterpret_cast<float*>(smem_raw + a.off_query);
-    m.part = reinterpret_cast<GcPart*>(smem_raw + a.off_part);
+    m.pos_d = reinterpret_cast<float*>(smem_raw + a.off_pos);
+    m.pos_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_pos) + a.R;
     m.ctl = reinterpret_cast<GcCtl*>(smem_raw + a.off_ctl);
     m.list_d = reinterpret_cast<float*>(smem_raw + a.off_list);
     m.list_i = reinterpret_cast<uint32_t*>(smem_raw + a.off_list + 32 * 4);
@@ -138,7 +134,6 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                                          const GcOut& o) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sq = m.sq;
-    GcPart* part = m.part;
     GcCtl* ctl = m.ctl;
     const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
     const float kInf = __int_as_float(0x7f800000);
@@ -171,19 +166,29 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     float rd = kInf;  // R_ij slot `lane` (warp 0)
     uint32_t ri = kInvalid;
     uint32_t t = 0;
-    // Pipelined hops (TMA staging, whole rows in one round): each warp's first group
-    // of the next hop is issued as soon as the next node is known — while warp 0 runs
+    // Pipelined hops (whole rows in one round): each evaluating warp's first slice of
+    // the next hop is issued as soon as the next node is known — while warp 0 runs
     // merge_halves — and completed at the top of the next hop.
     const bool pipe = a.ld <= a.dch && a.slots >= 32;  // TMA or LDGSTS split gathers
-    // evaluating warps: all, or warps 1.. when warp 0 is kept for combine + merge (then
-    // the next hop's first groups are issued by warps 1.. while warp 0 merges, and the
-    // merge leaves the hop's critical path)
+    // Evaluating warps: all, or warps 1.. when warp 0 is kept for combine + merge (its
+    // merge then overlaps their gathers).  The hop's edges are spread over them in
+    // slices of a.slice positions (warp ew takes positions r*nev*SL + ew*SL + [0, SL)
+    // in round r).  Measured on C2 (batch 1, t0=10): slices of 32 / 28 / 24 / 20 / 16 /
+    // 8 take 51 / 52 / 54 / 57 / 60 / 77 us — narrower slices push the ~58-edge
+    // prefix into a second, un-pipelined round — so the default is 32 (TSDG_GC_SLICE).
+    // Every evaluated position's distance lands in pos_d / pos_i and
+    // warp 0 forms R_temp from them in the reference's order: lane j keeps the
+    // strict-< minimum over positions j, j + 32, ... (lane_update, rank_list.cpp:8-18).
     const uint32_t ew0 = a.merge_warp ? 1u : 0u, nev = (uint32_t)kGcWarps - ew0;
     const bool evaluates = (uint32_t)warp >= ew0;
-    const uint32_t ew = evaluates ? (uint32_t)warp - ew0 : 0u;  // this warp's first group
-    const uint32_t j0 = evaluates ? ew * 32 + lane : 0xFFFFFFFFu;
+    const uint32_t ew = evaluates ? (uint32_t)warp - ew0 : 0u;
+    const uint32_t SL = a.slice, P = nev * SL;
+    const bool lane_on = evaluates && (uint32_t)lane < SL;
+    const uint32_t j0 = lane_on ? ew * SL + lane : 0xFFFFFFFFu;  // round-0 position
+    float* pos_d = m.pos_d;
+    uint32_t* pos_i = m.pos_i;
     uint32_t deg = 0, e0 = kInvalid;
-    bool pend = false;  // this lane's row of the pre-issued group
+    bool pend = false;  // this lane's row of the pre-issued slice
     if (pipe) {
         const uint32_t u = ctl->u;
         deg = __ldg(a.degcut + u);
@@ -200,52 +205,47 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         const uint32_t u = ctl->u;
         const uint32_t* arow = a.adj + (size_t)u * a.R;
         if (!pipe) {
-            // deg and this warp's first adjacency group load together (no deg -> row
+            // deg and this warp's first adjacency slice load together (no deg -> row
             // dependency on the hop's critical path)
             e0 = j0 < a.R ? __ldg(arow + j0) : kInvalid;
             deg = __ldg(a.degcut + u);
         }
         const uint32_t ngroups = (deg + 31) / 32;
-        float md = kInf;
-        uint32_t mi = kInvalid, mg = 0xFFFFFFFFu;
-        if (pipe) {  // the first group was issued during the previous hop's merge
+        if (pipe) {  // the first slice was issued during the previous hop's merge
             const float dist = gather_complete<METRIC, FAST, STAGE>(w, g, pend, lane);
-            if (pend && dist < md) {
-                md = dist;
-                mi = e0;
-                mg = ew;
+            if (pend) {
+                pos_d[j0] = dist;
+                pos_i[j0] = e0;
             }
             pend = false;
         }
-        for (uint32_t gi = pipe ? ew + nev : ew; evaluates && gi < ngroups; gi += nev) {
-            const uint32_t j = gi * 32 + lane;
-            const bool valid = j < deg;
-            const uint32_t e = valid ? (gi == ew ? e0 : __ldg(arow + j)) : kInvalid;
+        for (uint32_t r0 = pipe ? P : 0; evaluates && r0 < deg; r0 += P) {
+            const uint32_t j = r0 + ew * SL + lane;
+            const bool valid = lane_on && j < deg;
+            const uint32_t e = valid ? (r0 == 0 ? e0 : __ldg(arow + j)) : kInvalid;
             gc_prefetch_adj(a, valid, e);
             const float dist = gather_eval<METRIC, FAST, STAGE>(w, g, valid, e, lane);
-            if (valid && dist < md) {
-                md = dist;
-                mi = e;
-                mg = gi;
+            if (valid) {
+                pos_d[j] = dist;
+                pos_i[j] = e;
             }
         }
         PH_MARK(1)  // adjacency + gather + distances
-        part[warp * 32 + lane] = GcPart{md, mi, mg, 0};
         __syncthreads();
         PH_MARK(2)  // barrier: slowest warp's gather
-        // warp 0 combines the partials into R_temp and finds the next node, the
-        // minimum of R_temp (greedy_search.cpp:63-67) — known before merge_halves
+        // warp 0 forms R_temp and finds the next node, the minimum of R_temp
+        // (greedy_search.cpp:63-67) — known before merge_halves
         float td = kInf;
         uint32_t ti = kInvalid, ni = kInvalid;
         if (warp == 0) {
-            uint32_t tg = 0xFFFFFFFFu;
-            for (int ww = 0; ww < kGcWarps; ++ww) {
-                const GcPart p = part[ww * 32 + lane];
-                if (p.id == kInvalid) continue;
-                if (p.d < td || (p.d == td && p.group < tg)) {
-                    td = p.d;
-                    ti = p.id;
-                    tg = p.group;
+            for (uint32_t gi = 0; gi < ngroups; ++gi) {
+                const uint32_t j = gi * 32 + lane;
+                if (j < deg) {
+                    const float d = pos_d[j];
+                    if (d < td) {  // strict: an earlier group keeps a tie
+                        td = d;
+                        ti = pos_i[j];
+                    }
                 }
             }
             float nd = td;

@@ -584,6 +584,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.degcut = get_degcut(idx, p->lambda_cut, st);
     a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 0);  // measured: no gain (C2 batch 1/8/64)
     a.merge_warp = (uint32_t)env_int("TSDG_GC_MERGE_WARP", 1);
+    a.slice = a.merge_warp ? (uint32_t)std::max(1, std::min(32, env_int("TSDG_GC_SLICE", 32))) : 32u;
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
@@ -602,7 +603,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.off_ctl = c.take(sizeof(GcCtl));
     a.off_list = c.take(32 * 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_part = c.take(kGcThreads * sizeof(GcPart));
+    a.off_pos = c.take((size_t)idx->R * 8);
     a.off_stage = c.take(kGcWarps * a.slots * (a.dch + 4) * 4, 128);
     a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 + 2 * a.t0 * 4 : 0);
     a.off_rowid = c.take(kGcWarps * 32 * 4);
