@@ -707,6 +707,8 @@ def main():
         e2e_step()  # synchronous: returns after the D2H copies landed
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(e2e_times))
+    zero_copy = all(L.tsdg_gpu_host_buffer_mapped(ctypes.c_void_p(t.data_ptr()), t.numel() * t.element_size())
+                    for t in (hq, h_ids, h_d, h_c)) and os.environ.get("TSDG_ZERO_COPY", "1") != "0"
     e2e_val = total_q * args.steps / e2e_s
     assert np.array_equal(h_ids.numpy().view(np.uint32), head["ids"]), "e2e result differs"
 
@@ -780,7 +782,7 @@ def main():
                     "d2h_bytes_per_step": int(nq * k * 8 + nq * 4),
                     "host_cpus": f"{len(local_cpus)} GPU-local CPUs (NVML affinity)" if local_cpus else "all",
                     "transfer": "zero-copy (kernel reads/writes pinned host memory)"
-                    if os.environ.get("TSDG_ZERO_COPY", "1") != "0" else "copy pipeline (2 chunks, 2 streams)"},
+                    if zero_copy else "copy pipeline (2 chunks, 2 streams)"},
             "gpu_launches": head["launches"],
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

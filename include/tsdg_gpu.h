@@ -288,6 +288,11 @@ int tsdg_gpu_graph_destroy(tsdg_gpu_graph* g);
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t tsdg_gpu_launch_count(void);
 
+/* 1 when [p, p + bytes) lies in one mapped pinned host allocation — the condition
+ * under which the host-pointer search calls take the zero-copy path (the kernel reads
+ * queries from / writes results to host memory); 0 otherwise (copy pipeline). */
+int tsdg_gpu_host_buffer_mapped(const void* p, uint64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

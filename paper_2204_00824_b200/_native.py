@@ -45,6 +45,7 @@ SIGNATURES = {
     "tsdg_gpu_last_error": (ctypes.c_char_p, []),
     "tsdg_gpu_abi_version": (_I, []),
     "tsdg_gpu_launch_count": (_U64, []),
+    "tsdg_gpu_host_buffer_mapped": (_I, [_VP, _U64]),
     "tsdg_read_tsdg_header": (_I, [ctypes.c_char_p, _VP]),
     "tsdg_read_tsdg": (_I, [ctypes.c_char_p, _VP, _VP, _VP, _VP]),
     "tsdg_gpu_index_create": (_I, [_VP, _U32, _U32, _VP, _VP, _VP, _I, _I, _VP]),

@@ -1398,6 +1398,10 @@ const char* tsdg_gpu_last_error(void) { return g_err.c_str(); }
 int tsdg_gpu_abi_version(void) { return TSDG_GPU_ABI_VERSION; }
 uint64_t tsdg_gpu_launch_count(void) { return g_launches.load(); }
 
+int tsdg_gpu_host_buffer_mapped(const void* p, uint64_t bytes) {
+    return mapped_alias(p, (size_t)bytes) != nullptr ? 1 : 0;
+}
+
 int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint64_t* offsets,
                           const uint32_t* targets, const uint16_t* lambdas, int metric,
                           int device, tsdg_gpu_index** out) {
