@@ -20,6 +20,24 @@
  * TSDG_MODE_FAST is allowed to differ in fp32 rounding of distances only
  * (fused multiply-add, tree reduction); its recall must stay within 0.5 points
  * of the reference at equal parameters.
+ *
+ * Environment (read at each call; defaults are the measured best on C2, and none of
+ * them changes deterministic-mode results):
+ *   TSDG_ZERO_COPY=0        host-pointer calls use the copy pipeline even when every
+ *                           buffer is mapped pinned memory
+ *   TSDG_E2E_CHUNKS, TSDG_E2E_FIRST   copy-pipeline chunking (2 chunks, first 25%)
+ *   TSDG_FAST_KERNEL=staged|register  fast best-first kernel choice (default: the
+ *                           register-direct kernel for rows <= 128 floats, k <= 31)
+ *   TSDG_FAST_PAIR=0|1      force the single / paired (two warps per query) fast
+ *                           kernel (default: paired below one query per CTA slot)
+ *   TSDG_FAST_VARIANT, TSDG_FAST_PREFETCH   fast-kernel tuning variants (bf_fast.cu)
+ *   TSDG_STAGE=ldgsts, TSDG_SLOTS, TSDG_BF_WARPS, TSDG_PREFETCH, TSDG_BATCH_MIN
+ *                           staged best-first kernel: staging path / slots / warps
+ *   TSDG_GREEDY=cta|warp, TSDG_GREEDY_CTA_MAX_WALKS   greedy kernel routing
+ *   TSDG_GC_STAGE=ldgsts, TSDG_GC_MERGE_WARP, TSDG_GC_SLICE, TSDG_GC_ADJ_PREFETCH,
+ *   TSDG_GR_WARPS           greedy kernels' staging / warp roles
+ *   TSDG_SCAN_SPLITS        exact-scan base splits
+ *   TSDG_DEBUG_PATH=1, TSDG_LOAD_TRACE=1   diagnostics on stderr
  */
 #ifndef TSDG_GPU_H
 #define TSDG_GPU_H
