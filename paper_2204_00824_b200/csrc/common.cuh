@@ -34,6 +34,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (threadIdx.x == 0 && blockIdx.x < 256 && (i) < 32)                           \
             tsdg_dev::g_trace[blockIdx.x][(i)] = tsdg_dev::gtimer();                    \
     }
+// Per-hop, per-warp event trace of CTA 0 of the greedy cluster kernel (globaltimer):
+// g_hop[warp][hop][event] (tools/hop_trace.py).
+__device__ unsigned long long g_hop[4][32][8];
+#define HOP_MARK(t, i)                                                                  \
+    {                                                                                   \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (t) < 32 && (threadIdx.x >> 5) < 4) \
+            tsdg_dev::g_hop[threadIdx.x >> 5][(t)][(i)] = tsdg_dev::gtimer();           \
+    }
 #define PH_DECL long long _ph = clock64();
 #define PH_RESET _ph = clock64();
 #define PH_MARK(i)                                                                      \
@@ -47,6 +55,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PH_RESET
 #define PH_MARK(i)
 #define TR_MARK(i)
+#define HOP_MARK(t, i)
 #endif
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;

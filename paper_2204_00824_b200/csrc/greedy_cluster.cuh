@@ -202,6 +202,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     PH_MARK(0)  // phase 0: query load + select_start
     while (ctl->improved && t < a.hop_limit) {
         ++t;
+        HOP_MARK(t, 0)
         const uint32_t u = ctl->u;
         const uint32_t* arow = a.adj + (size_t)u * a.R;
         if (!pipe) {
@@ -218,6 +219,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                 pos_i[j0] = e0;
             }
             pend = false;
+            HOP_MARK(t, 1)
         }
         for (uint32_t r0 = pipe ? P : 0; evaluates && r0 < deg; r0 += P) {
             const uint32_t j = r0 + ew * SL + lane;
@@ -231,7 +233,9 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             }
         }
         PH_MARK(1)  // adjacency + gather + distances
+        HOP_MARK(t, 2)
         __syncthreads();
+        HOP_MARK(t, 3)
         PH_MARK(2)  // barrier: slowest warp's gather
         // warp 0 forms R_temp and finds the next node, the minimum of R_temp
         // (greedy_search.cpp:63-67) — known before merge_halves
@@ -254,6 +258,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             if (lane == 0) ctl->u_next = ni;
         }
         __syncthreads();
+        HOP_MARK(t, 4)
         const uint32_t un = ctl->u_next;
         // next hop (wasted only if the walk stops here): deg + this warp's first group
         uint32_t ndeg = 0, ne = kInvalid;
@@ -268,6 +273,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                 ctl->improved = updated ? 1u : 0u;
                 ctl->evals += deg;
             }
+            HOP_MARK(t, 5)
         } else if (!pipe && un != kInvalid) {
             // while warp 0 merges, the other warps pull the next hop's deg_cut entry,
             // adjacency row and neighbour rows into L2 (wasted only on the last hop)
@@ -284,14 +290,17 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             pend = j0 < ndeg;
             e0 = pend ? ne : kInvalid;
             if (e0 == 0xFFFFFFFEu) asm volatile("" ::: "memory");  // (phases build: e0 loaded)
+            if (warp != 0) HOP_MARK(t, 5)
             PH_MARK(3)  // combine + (warp 0) merge_halves / (others) next adjacency
             gather_issue_s<STAGE>(w, g, pend, e0, lane);
             gc_prefetch_adj(a, pend, e0);
             PH_MARK(5)  // next hop's row copies issued
+            HOP_MARK(t, 6)
         } else {
             PH_MARK(3)
         }
         __syncthreads();
+        HOP_MARK(t, 7)
         TR_MARK(3 + t)
         PH_MARK(4)  // barrier
     }

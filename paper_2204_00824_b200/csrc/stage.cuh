@@ -289,10 +289,26 @@ __device__ __forceinline__ void gather_issue_ldgsts(WarpStage& w, const Geom& g,
     __syncwarp();
     const uint32_t nvec = g.ld >> 2, rpi = 32u / nvec;
     const uint32_t sub = (uint32_t)lane / nvec, piece = (uint32_t)lane % nvec;
-    for (uint32_t t = 0; t < cnt; t += rpi) {
-        const uint32_t row = t + sub;
-        if (sub < rpi && row < cnt)
-            cp_async16(w.stage + row * pitch + piece * 4, g.vec + (size_t)w.rowid[row] * g.ld + piece * 4);
+    if (nvec == 32) {
+        // one 512-B row per warp instruction; the row ids come from registers
+        // (shuffles), so successive copies do not wait on each other: no "memory"
+        // clobber between them (the staging slots are read only after the
+        // cp.async.wait_group in gather_complete, which carries one)
+        const uint32_t rid = w.rowid[lane];
+        const float* src = g.vec + piece * 4;
+        float* dst = w.stage + piece * 4;
+#pragma unroll 8
+        for (uint32_t r = 0; r < cnt; ++r) {
+            const uint32_t id = __shfl_sync(kFull, rid, (int)r);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + r * pitch)),
+                         "l"(src + (size_t)id * g.ld));
+        }
+    } else {
+        for (uint32_t t = 0; t < cnt; t += rpi) {
+            const uint32_t row = t + sub;
+            if (sub < rpi && row < cnt)
+                cp_async16(w.stage + row * pitch + piece * 4, g.vec + (size_t)w.rowid[row] * g.ld + piece * 4);
+        }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }

@@ -2303,6 +2303,12 @@ extern "C" int tsdg_gpu_trace_read(unsigned long long* out) {
     cudaMemcpyToSymbol(tsdg_dev::g_trace, zero, sizeof(zero));
     return 0;
 }
+extern "C" int tsdg_gpu_hop_trace_read(unsigned long long* out) {  // 4 x 32 x 8 u64, reset after
+    if (cudaMemcpyFromSymbol(out, tsdg_dev::g_hop, 4 * 32 * 8 * 8) != cudaSuccess) return 2;
+    static unsigned long long zero[4][32][8];
+    cudaMemcpyToSymbol(tsdg_dev::g_hop, zero, sizeof(zero));
+    return 0;
+}
 extern "C" int tsdg_gpu_phase_read(unsigned long long* out8, int reset) {
     static unsigned long long host[1 << 16][8];
     if (cudaMemcpyFromSymbol(host, tsdg_dev::g_phase, sizeof(host)) != cudaSuccess) return 2;
