@@ -55,6 +55,17 @@ struct GrArgs {
 // subsequence of the sorted R_temp), so instead of sorting 64 keys the warp forms
 // the bitonic sequence R_ij ++ reverse(newcomers), keeps the lower half of one
 // half-cleaner step (the 32 smallest) and sorts it with 5 more steps.
+// Index of the n-th (0-based) set bit of m, which has more than n bits set: the
+// largest p with popc(m below p) <= n, by a 5-step binary search (no __fns loop).
+__device__ __forceinline__ int nth_set_bit(unsigned m, unsigned n) {
+    int pos = 0;
+#pragma unroll
+    for (int b = 16; b > 0; b >>= 1) {
+        if ((unsigned)__popc(m & ((1u << (pos + b)) - 1u)) <= n) pos += b;
+    }
+    return pos;
+}
+
 __device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float td,
                                                   uint32_t ti, int lane) {
     warp_sort32(td, ti, lane);  // incoming, ascending
@@ -67,7 +78,7 @@ __device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float
     // lane L takes newcomer number 31 - L (the reversed, compacted newcomer list)
     const uint32_t want = 31u - (uint32_t)lane;
     const bool has = want < (uint32_t)__popc(vm);
-    const int src = has ? (int)__fns(vm, 0, (int)want + 1) : 0;
+    const int src = has ? nth_set_bit(vm, want) : 0;
     const float sd = __shfl_sync(kFull, td, src);
     const uint32_t sid = __shfl_sync(kFull, ti, src);
     float nd = rd;
