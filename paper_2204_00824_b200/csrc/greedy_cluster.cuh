@@ -52,6 +52,7 @@ struct GcArgs {
     uint32_t merge_warp;    // 1: warp 0 only combines / merges, warps 1.. evaluate the
                             // hop's edges (its merge then overlaps their gathers)
     uint32_t slice;         // edges per evaluating warp per round (16 or 32)
+    uint32_t early_next;    // 1: next node from the evaluating warps' minima
     uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
                             // evaluated node (the next hop's u is one of them)
     uint32_t npow2;      // pool size for the in-cluster merge
@@ -65,7 +66,19 @@ struct GcCtl {
     uint32_t hops;
     uint32_t evals;
     uint32_t u_next;  // next node, published before the merge (L2 warm-up)
+    // per evaluating warp: its smallest distance of the hop (orderable key), the id
+    // holding it and how many candidates share it (the early next-node pick)
+    uint32_t best_k[4];
+    uint32_t best_i[4];
+    uint32_t best_n[4];
 };
+
+// float -> uint32 with the same order (closer() on distances; -0 == +0)
+__device__ __forceinline__ uint32_t gc_fkey(float d) {
+    uint32_t b = __float_as_uint(d);
+    if ((b << 1) == 0) b = 0;
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
 
 __device__ __forceinline__ void cluster_arrive_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -212,12 +225,31 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             deg = __ldg(a.degcut + u);
         }
         const uint32_t ngroups = (deg + 31) / 32;
+        // this warp's smallest distance of the hop (one REDUX per round), its holder
+        // and its multiplicity
+        uint32_t bk = 0xFFFFFFFFu, bi = kInvalid, bn = 0;
+        auto track = [&](bool valid, float dist, uint32_t e) {
+            const uint32_t key = valid ? gc_fkey(dist) : 0xFFFFFFFFu;
+            const uint32_t mk = __reduce_min_sync(kFull, key);
+            const unsigned hit = __ballot_sync(kFull, valid && key == mk);
+            if (hit == 0u) return;  // warp-uniform
+            const uint32_t mi = __shfl_sync(kFull, e, __ffs(hit) - 1);
+            if (mk < bk) {
+                bk = mk;
+                bi = mi;
+                bn = __popc(hit);
+            } else if (mk == bk) {
+                bn += __popc(hit);
+                bi = min(bi, mi);
+            }
+        };
         if (pipe) {  // the first slice was issued during the previous hop's merge
             const float dist = gather_complete<METRIC, FAST, STAGE>(w, g, pend, lane);
             if (pend) {
                 pos_d[j0] = dist;
                 pos_i[j0] = e0;
             }
+            if (a.early_next && evaluates) track(pend, dist, e0);
             pend = false;
             HOP_MARK(t, 1)
         }
@@ -231,14 +263,43 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                 pos_d[j] = dist;
                 pos_i[j] = e;
             }
+            if (a.early_next) track(valid, dist, e);
+        }
+        if (a.early_next && evaluates && lane == 0) {
+            ctl->best_k[ew] = bk;
+            ctl->best_i[ew] = bi;
+            ctl->best_n[ew] = bn;
         }
         PH_MARK(1)  // adjacency + gather + distances
         HOP_MARK(t, 2)
         __syncthreads();
         HOP_MARK(t, 3)
         PH_MARK(2)  // barrier: slowest warp's gather
-        // warp 0 forms R_temp and finds the next node, the minimum of R_temp
-        // (greedy_search.cpp:63-67) — known before merge_halves
+        // The next node is the minimum of R_temp by closer (greedy_search.cpp:63-67).
+        // When the hop's smallest distance is held by exactly one candidate, that
+        // candidate wins its lane slot (nothing before it in the slot is as close) and
+        // is the minimum of R_temp: every warp takes it from the evaluating warps'
+        // minima right after the barrier and starts the next adjacency load while warp
+        // 0 forms R_temp and merges.  A tie at the minimum falls back to warp 0's
+        // selection from R_temp (one more barrier).
+        uint32_t un = kInvalid;
+        bool early = false;
+        if (a.early_next) {
+            uint32_t gk = 0xFFFFFFFFu, gid = kInvalid, gn = 0;
+            for (uint32_t v = 0; v < nev; ++v) {
+                const uint32_t k2 = ctl->best_k[v];
+                if (k2 < gk) {
+                    gk = k2;
+                    gid = ctl->best_i[v];
+                    gn = ctl->best_n[v];
+                } else if (k2 == gk) {
+                    gn += ctl->best_n[v];
+                }
+            }
+            early = gn == 1u;  // CTA-uniform
+            un = gid;
+        }
+        // warp 0 forms R_temp (and, without the early pick, the next node)
         float td = kInf;
         uint32_t ti = kInvalid, ni = kInvalid;
         if (warp == 0) {
@@ -252,14 +313,20 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                     }
                 }
             }
-            float nd = td;
-            ni = ti;
-            warp_argmin(nd, ni);
-            if (lane == 0) ctl->u_next = ni;
+            if (early) {
+                ni = un;  // the minimum of R_temp (see above)
+            } else {
+                float nd = td;
+                ni = ti;
+                warp_argmin(nd, ni);
+                if (lane == 0) ctl->u_next = ni;
+            }
         }
-        __syncthreads();
+        if (!early) {
+            __syncthreads();
+            un = ctl->u_next;
+        }
         HOP_MARK(t, 4)
-        const uint32_t un = ctl->u_next;
         // next hop (wasted only if the walk stops here): deg + this warp's first group
         uint32_t ndeg = 0, ne = kInvalid;
         if (pipe && un != kInvalid) {

@@ -585,6 +585,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.adj_prefetch = (uint32_t)env_int("TSDG_GC_ADJ_PREFETCH", 0);  // measured: no gain (C2 batch 1/8/64)
     a.merge_warp = (uint32_t)env_int("TSDG_GC_MERGE_WARP", 1);
     a.slice = a.merge_warp ? (uint32_t)std::max(1, std::min(32, env_int("TSDG_GC_SLICE", 32))) : 32u;
+    a.early_next = (uint32_t)env_int("TSDG_GC_EARLY", 1);
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
