@@ -51,11 +51,12 @@ __device__ unsigned long long g_hop[4][32][8];
         _ph = _n;                                                                       \
     }
 #else
+// empty statements (not nothing): `if (c) PH_MARK(i)` must not capture the next line
 #define PH_DECL
 #define PH_RESET
-#define PH_MARK(i)
-#define TR_MARK(i)
-#define HOP_MARK(t, i)
+#define PH_MARK(i) {}
+#define TR_MARK(i) {}
+#define HOP_MARK(t, i) {}
 #endif
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;

@@ -357,7 +357,9 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             pend = j0 < ndeg;
             e0 = pend ? ne : kInvalid;
             if (e0 == 0xFFFFFFFEu) asm volatile("" ::: "memory");  // (phases build: e0 loaded)
-            if (warp != 0) HOP_MARK(t, 5)
+            if (warp != 0) {
+                HOP_MARK(t, 5)
+            }
             PH_MARK(3)  // combine + (warp 0) merge_halves / (others) next adjacency
             gather_issue_s<STAGE>(w, g, pend, e0, lane);
             gc_prefetch_adj(a, pend, e0);

@@ -341,3 +341,30 @@ def test_greedy_kernels_bit_exact(orc, fixtures, index, golden, golden_meta, mon
             want = orc.small_batch(g, b, q[:16], 10, p)
             np.testing.assert_array_equal(got.ids, want.ids)
             np.testing.assert_array_equal(got.dists.view(np.uint32), want.dists.view(np.uint32))
+
+
+@pytest.mark.parametrize("merge_warp,early,stage", [("0", "0", "tma"), ("1", "0", "tma"), ("1", "1", "tma"),
+                                                    ("1", "1", "ldgsts"), ("1", "0", "ldgsts")])
+def test_greedy_cluster_kernel_variants_bit_exact(orc, fixtures, index, golden, golden_meta, monkeypatch,
+                                                  merge_warp, early, stage):
+    """The greedy cluster kernel's internal variants — warp 0 merging while warps 1-3
+    gather (TSDG_GC_MERGE_WARP), the early next-node pick (TSDG_GC_EARLY), TMA or
+    cp.async row staging (TSDG_GC_STAGE) — all reproduce the reference."""
+    monkeypatch.setenv("TSDG_GREEDY", "cta")
+    monkeypatch.setenv("TSDG_GC_MERGE_WARP", merge_warp)
+    monkeypatch.setenv("TSDG_GC_EARLY", early)
+    monkeypatch.setenv("TSDG_GC_STAGE", stage)
+    for name in FIXTURES:
+        g, b, q = fixtures(name)
+        idx = index(name)
+        for i, gd in enumerate(golden_meta["gr_grid"]):
+            p = GreedyParams(**{k: v for k, v in gd.items() if k != "k"})
+            got = idx.search_greedy(q[:48], gd["k"], p)
+            np.testing.assert_array_equal(got.ids, golden[f"{name}_gr{i}_ids"][:48])
+            np.testing.assert_array_equal(got.stats["hops"], golden[f"{name}_gr{i}_stats"][:48, 0])
+            np.testing.assert_array_equal(got.stats["distance_evals"], golden[f"{name}_gr{i}_stats"][:48, 1])
+        p = GreedyParams(t0=12, hop_limit=3, seed=9)  # hop limit reached mid-walk
+        want = orc.small_batch(g, b, q[:24], 10, p)
+        got = idx.search_greedy(q[:24], 10, p)
+        np.testing.assert_array_equal(got.ids, want.ids)
+        np.testing.assert_array_equal(got.dists.view(np.uint32), want.dists.view(np.uint32))
