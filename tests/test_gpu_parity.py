@@ -343,10 +343,12 @@ def test_greedy_kernels_bit_exact(orc, fixtures, index, golden, golden_meta, mon
             np.testing.assert_array_equal(got.dists.view(np.uint32), want.dists.view(np.uint32))
 
 
-@pytest.mark.parametrize("merge_warp,early,stage", [("0", "0", "tma"), ("1", "0", "tma"), ("1", "1", "tma"),
-                                                    ("1", "1", "ldgsts"), ("1", "0", "ldgsts")])
+@pytest.mark.parametrize("merge_warp,early,stage,extra", [
+    ("0", "0", "tma", {}), ("0", "1", "ldgsts", {}), ("1", "0", "tma", {}), ("1", "1", "tma", {}),
+    ("1", "1", "ldgsts", {}), ("1", "0", "ldgsts", {}),
+    ("1", "1", "tma", {"TSDG_GC_SLICE": "16"}), ("1", "1", "tma", {"TSDG_GC_ADJ_PREFETCH": "1"})])
 def test_greedy_cluster_kernel_variants_bit_exact(orc, fixtures, index, golden, golden_meta, monkeypatch,
-                                                  merge_warp, early, stage):
+                                                  merge_warp, early, stage, extra):
     """The greedy cluster kernel's internal variants — warp 0 merging while warps 1-3
     gather (TSDG_GC_MERGE_WARP), the early next-node pick (TSDG_GC_EARLY), TMA or
     cp.async row staging (TSDG_GC_STAGE) — all reproduce the reference."""
@@ -354,6 +356,8 @@ def test_greedy_cluster_kernel_variants_bit_exact(orc, fixtures, index, golden, 
     monkeypatch.setenv("TSDG_GC_MERGE_WARP", merge_warp)
     monkeypatch.setenv("TSDG_GC_EARLY", early)
     monkeypatch.setenv("TSDG_GC_STAGE", stage)
+    for k, v in extra.items():
+        monkeypatch.setenv(k, v)
     for name in FIXTURES:
         g, b, q = fixtures(name)
         idx = index(name)
