@@ -293,3 +293,44 @@ def test_fast_paired_kernel_equals_single_on_fixtures(fixtures, index, monkeypat
             res[pair] = idx.search_bestfirst(q, p, mode=_native.MODE_FAST)
         np.testing.assert_array_equal(res["1"].ids, res["0"].ids)
         np.testing.assert_array_equal(res["1"].dists.view(np.uint32), res["0"].dists.view(np.uint32))
+
+
+@pytest.mark.parametrize("env", [{"TSDG_FAST_VARIANT": str(v)} for v in range(8)]
+                         + [{"TSDG_FAST_PREFETCH": p} for p in ("0", "2", "5")]
+                         + [{"TSDG_FAST_KERNEL": "staged"}, {"TSDG_FAST_KERNEL": "register"}])
+def test_fast_kernel_knobs_keep_recall(fixtures, index, golden, monkeypatch, env):
+    """Every compiled fast-kernel variant / prefetch mode / kernel choice runs and keeps
+    recall@1 and @10 within 0.5 pt of the deterministic (reference) result."""
+    from paper_2204_00824_b200.search import BestFirstParams
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for name in ("syn2k", "lowlid3k"):
+        g, b, q = fixtures(name)
+        idx = index(name)
+        gt = golden[f"{name}_gt"]
+        p = BestFirstParams(k=12, seed=5)
+        det = idx.search_bestfirst(q, p)
+        fast = idx.search_bestfirst(q, p, mode=_native.MODE_FAST)
+        for kk in (1, 10):
+            assert abs(O.recall_at_k(fast.ids, fast.counts, gt, kk)
+                       - O.recall_at_k(det.ids, det.counts, gt, kk)) <= 0.005, (env, name, kk)
+    if datasets.available("c1_lowlid_100k"):  # d = 128: the row class the variants target
+        from paper_2204_00824_b200 import search
+        ds = _c1()
+        p = BestFirstParams(k=14, seed=7)
+        det = ds[1].search_bestfirst(ds[0].queries, p)
+        fast = ds[1].search_bestfirst(ds[0].queries, p, mode=_native.MODE_FAST)
+        for kk in (1, 10):
+            assert abs(O.recall_at_k(fast.ids, fast.counts, ds[0].gt, kk)
+                       - O.recall_at_k(det.ids, det.counts, ds[0].gt, kk)) <= 0.005, (env, "c1", kk)
+
+
+_C1 = []
+
+
+def _c1():
+    if not _C1:
+        from paper_2204_00824_b200 import search
+        ds = datasets.load("c1_lowlid_100k")
+        _C1.append((ds, search.GpuIndex.from_file(ds.graph_path, ds.base)))
+    return _C1[0]
