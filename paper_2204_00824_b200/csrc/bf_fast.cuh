@@ -23,8 +23,9 @@
 //     size fields: membership is 8 LDS.128 + compares with no branches, a full
 //     segment is "slot 31 is not the sentinel", the FIFO write slot of a V segment
 //     is (adds to that segment) mod 32 held in lane s's register;
-//   * rows past the first batch of a hop are pulled into L2 by one bulk prefetch
-//     per row (cp.async.bulk.prefetch.L2, UBLKPF) as soon as the hop's needed set
+//   * rows past the first batch of a hop are pulled into L2 by per-lane 128-byte
+//     line prefetches (row_prefetch; a bulk prefetch per row is the slower option)
+//     as soon as the hop's needed set
 //     is known, so only the first batch waits on DRAM (C2: 0.85 -> 0.79 ms);
 //   * per-warp shared memory drops from 12.7 KB to ~4.5 KB (d = 128, m = 8).
 //
