@@ -213,10 +213,18 @@ __device__ __forceinline__ uint32_t warp_kway_unique(const float* ld, const uint
     }
     uint32_t cnt = 0;
     while (cnt < k) {
-        float bd = hd;
-        uint32_t bi = hi;
-        warp_argmin(bd, bi);
-        if (bi == kInvalid) break;
+        // closer()-minimum of the heads by two REDUX.MIN: the distance (as an
+        // order-preserving key; -0 == +0), then the smallest id holding it
+        uint32_t kd = 0xFFFFFFFFu;
+        if (hi != kInvalid) {
+            uint32_t b = __float_as_uint(hd);
+            if ((b << 1) == 0) b = 0;
+            kd = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+        }
+        const uint32_t mk = __reduce_min_sync(kFull, kd);
+        if (mk == 0xFFFFFFFFu) break;  // every list exhausted
+        const uint32_t bi = __reduce_min_sync(kFull, kd == mk ? hi : 0xFFFFFFFFu);
+        const float bd = __shfl_sync(kFull, hd, __ffs(__ballot_sync(kFull, kd == mk && hi == bi)) - 1);
         out(cnt, bi, bd);
         ++cnt;
         if (hi == bi) {

@@ -417,11 +417,8 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
                 hsum += m.walk_cnt[2 * r];
                 esum += m.walk_cnt[2 * r + 1];
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                hsum += __shfl_xor_sync(kFull, hsum, off);
-                esum += __shfl_xor_sync(kFull, esum, off);
-            }
+            hsum = __reduce_add_sync(kFull, hsum);
+            esum = __reduce_add_sync(kFull, esum);
         }
         uint32_t c = 0;
         if (a.k <= 64 && a.t0 <= 32) {
