@@ -86,17 +86,19 @@ __device__ __forceinline__ bool closer(float da, uint32_t ia, float db, uint32_t
     return ia < ib;
 }
 
-// Warp arg-min by closer(); every lane gets the winner.
+// Warp arg-min by closer(); every lane gets the winner.  Two REDUX.MIN (the distance
+// as an order-preserving key, -0 == +0 as in closer(); then the smallest id holding
+// that distance) and one shuffle for the winner's distance bits, instead of a 5-step
+// shuffle butterfly.
 __device__ __forceinline__ void warp_argmin(float& d, uint32_t& id) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const float od = __shfl_xor_sync(kFull, d, off);
-        const uint32_t oi = __shfl_xor_sync(kFull, id, off);
-        if (closer(od, oi, d, id)) {
-            d = od;
-            id = oi;
-        }
-    }
+    uint32_t b = __float_as_uint(d);
+    if ((b << 1) == 0) b = 0;
+    const uint32_t key = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    const uint32_t mk = __reduce_min_sync(kFull, key);
+    const uint32_t mi = __reduce_min_sync(kFull, key == mk ? id : 0xFFFFFFFFu);
+    const unsigned who = __ballot_sync(kFull, key == mk && id == mi);
+    d = __shfl_sync(kFull, d, __ffs(who) - 1);
+    id = mi;
 }
 
 // compare-exchange keeping min (keep_min) or max of (d,id) vs partner's
