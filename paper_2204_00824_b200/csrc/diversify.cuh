@@ -32,7 +32,7 @@ struct DivArgs {
     const float* vec;  // n x ld
     uint32_t n, d, ld;
     int metric;
-    unsigned long long keep;  // all ones (opaque())
+    unsigned long long keep;  // all ones; its sign bits give the opaque (-0, -0) addend
     // stage 1
     const uint32_t* knn_ids;  // n x k
     const float* knn_dists;
@@ -113,6 +113,9 @@ __device__ __forceinline__ void div_tile(const DivArgs& a, DivStage& st, const u
         __syncthreads();
         if (c0 + kDivDC < a.d) load(c0 + kDivDC);
         const uint32_t dims = min(kDivDC, a.d - c0);
+        // (-0, -0) from the arguments: fma(x, y, nz) is x * y rounded once and stays a
+        // separate rounding from the add (exact_scan.cuh scan_step)
+        const unsigned long long nz = a.keep & 0x8000000080000000ull;
         for (uint32_t t = 0; t < dims; ++t) {
             const ulonglong2* ip = reinterpret_cast<const ulonglong2*>(&st.is[t][8 * ti]);
             const ulonglong2 i01 = ip[0], i23 = ip[1], i45 = ip[2], i67 = ip[3];
@@ -127,11 +130,11 @@ __device__ __forceinline__ void div_tile(const DivArgs& a, DivStage& st, const u
                     unsigned long long tt;
                     if (METRIC == 0) {
                         const unsigned long long df = f2_sub(iv[r], jv[c]);
-                        tt = f2_mul(df, df);
+                        tt = f2_fma(df, df, nz);
                     } else {
-                        tt = f2_mul(iv[r], jv[c]);
+                        tt = f2_fma(iv[r], jv[c], nz);
                     }
-                    acc[r][c] = f2_add(acc[r][c], opaque(tt, a.keep));
+                    acc[r][c] = f2_add(acc[r][c], tt);
                 }
             }
         }

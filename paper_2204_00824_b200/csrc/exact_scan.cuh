@@ -10,63 +10,71 @@
 // expressed on tcgen05.  The packed f32x2 pipe (FADD2/FMUL2 — one rounding per
 // element, so still exact) gives two pair-dims per lane per instruction.
 //
-//   CTA = 32 queries x one split of the base rows; 256 threads, 8 warps.
-//   Base tile of 128 rows, dims in chunks of 32: the chunk is loaded to registers
-//   (LDG.128, next chunk in flight while the current one is reduced) and stored
-//   transposed (dim-major) in shared memory; queries the same way, each value
-//   duplicated as an (x, x) pair so one LDS.128 yields two packed operands.
-//   Thread (tq, tb) owns queries 2tq, 2tq+1 x rows {4tb..4tb+3, 64+4tb..64+4tb+3}:
-//   8 packed accumulators (16 pair distances) whose per-dim update is 8 SUB2 +
-//   8 MUL2 (L2) + 8 ADD2 (+ 16 ALU-pipe LOP3, see opaque()) for 3 LDS.128.
+//   CTA = 32 queries x one split of the base rows; 128 threads, 4 warps.
+//   Base tile of 128 rows, dims in chunks of 32, double-buffered: the rows go
+//   straight to shared memory row-major (cp.async, 16 B per lane, coalesced), the
+//   query chunk dim-major through registers.  Thread (tq, tb) owns queries
+//   4tq..4tq+3 x rows tb + 16i (i < 8): 16 packed accumulators, each an even/odd
+//   query pair against one row.  The row value is the scalar operand of the packed
+//   SUB2 (ptxas encodes the (x, x) broadcast as an operand modifier, `R.F32`), so
+//   per 4 dims a thread issues 8 + 4 LDS.128 for 192 packed FP instructions
+//   (16 x (SUB2 + FFMA2-with-(-0) + ADD2) per dim, see scan_step) — three times the
+//   FP work per shared-memory access of the round-1 layout, which was bound by its
+//   barriers and LSU, and no ALU-pipe masking.
+//   One barrier per chunk: the next chunk's loads are issued right after it, into
+//   the buffer every thread has finished with.
 //   After a tile, pairs closer than the query's current k-th (a stale, looser bound
 //   is fine) are appended to the query's candidate buffer (P entries in shared
-//   memory); when a buffer could overflow on the next tile it is sorted (warp
-//   bitonic) and cut to k, which also tightens the bound.  The split's final top-k
+//   memory); when a buffer could overflow on the next tile its new entries are
+//   sorted and merged into the sorted prefix, cut to k (scan_compact), which also
+//   tightens the bound.  The split's final top-k
 //   goes to global memory; splits are merged per query by merge_splits_kernel.
 #pragma once
 
-#include "stage.cuh"  // f32x2 helpers
+#include "stage.cuh"  // f32x2 helpers, cp_async16
 
 namespace tsdg_dev {
 
 constexpr uint32_t kScanQT = 32;        // queries per CTA
 constexpr uint32_t kScanBT = 128;       // base rows per tile
 constexpr uint32_t kScanDC = 32;        // dims per chunk
-constexpr uint32_t kScanThreads = 256;
-constexpr uint32_t kScanBPitch = kScanBT + 4;  // floats per dim row of the base tile
+constexpr uint32_t kScanThreads = 128;
+constexpr uint32_t kScanRPitch = kScanDC + 4;  // floats per staged row (conflict-free LDS.128)
+constexpr uint32_t kScanRowBuf = kScanBT * kScanRPitch;  // floats per row buffer
+constexpr uint32_t kScanQBuf = kScanDC * kScanQT;        // floats per query buffer
+
+constexpr uint32_t kScanSortN = 128;  // per-warp sort scratch (entries)
+
+// Dynamic shared memory of exact_scan_kernel for candidate buffers of P entries.
+constexpr size_t scan_smem_bytes(uint32_t P) {
+    return 2 * (size_t)(kScanRowBuf + kScanQBuf) * 4 + (size_t)kScanQT * P * 8 +
+           (size_t)(kScanThreads / 32) * kScanSortN * 8 + kScanQT * 16;
+}
 
 struct ScanArgs {
-    const float* base;      // n rows, stride ld_b floats (ld_b % 4 == 0)
+    const float* base;      // n rows, stride ld_b floats (ld_b % 4 == 0, 16-byte aligned)
     const float* queries;   // nq rows, stride ld_q floats (ld_q % 4 == 0)
     uint32_t n, nq, d, ld_b, ld_q;
     uint32_t k;             // results per query
-    uint32_t P;             // candidate buffer entries per query (power of 2, >= k + BT)
+    uint32_t P;             // candidate buffer entries per query (k + BT)
     uint32_t rows_per_split;
     uint64_t self_base;     // exclude_self: query q is base row self_base + q
     int exclude_self;
-    unsigned long long keep;  // all ones (host); see opaque()
+    unsigned long long keep;  // all ones (host); nz = keep & sign bits, see scan_step()
     uint32_t* out_ids;      // [split][nq][k]
     float* out_dists;
 };
 
 __device__ __forceinline__ unsigned long long f2_dup(float x) {
-    return (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(x) << 32);
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+    return r;
 }
 __device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
     unsigned long long r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
-// ptxas contracts a packed mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2 (a
-// single rounding: not the reference's value).  Masking the product with a value it
-// cannot see (all ones, from the kernel arguments) keeps the two roundings; the two
-// LOP3 run on the ALU pipe, off the FMA pipe this loop is bound by.
-__device__ __forceinline__ unsigned long long opaque(unsigned long long x, unsigned long long keep) {
-    unsigned long long r;
-    asm("and.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(keep));
-    return r;
-}
-
 // Ascending bitonic sort by closer() of P entries (power of 2) in shared memory, one
 // warp.
 __device__ __forceinline__ void warp_sort_smem(float* dd, uint32_t* ii, uint32_t P, int lane) {
@@ -90,15 +98,92 @@ __device__ __forceinline__ void warp_sort_smem(float* dd, uint32_t* ii, uint32_t
     }
 }
 
+// Compaction of one query's candidate buffer (one warp): entries [0, sorted) are the
+// sorted best-so-far (<= k), [sorted, cnt) new unsorted appends.  The new entries are
+// taken in batches of up to kScanSortN: sorted in the warp's scratch (bitonic over the
+// next power of 2), then merged with the sorted prefix by co-rank search, keeping the
+// first min(k, .) — the same set and order as sorting the whole buffer, at a fraction
+// of the cost once the prefix holds k entries and few rows pass the bound per tile.
+// A batch's merge output [0, nk) never reaches the unread appends (nk <= prefix +
+// batch).
+__device__ __forceinline__ void scan_compact(float* dd, uint32_t* ii, uint32_t sorted, uint32_t cnt,
+                                             uint32_t k, float* sd, uint32_t* si, uint32_t lane) {
+    const float kInf = __int_as_float(0x7f800000);
+    constexpr int kOut = (384 + 31) / 32;  // outputs per lane (k <= 384)
+    for (uint32_t b0 = sorted; b0 < cnt; b0 += kScanSortN) {
+        const uint32_t m = min(kScanSortN, cnt - b0);
+        uint32_t M = 2;
+        while (M < m) M <<= 1;
+        for (uint32_t i = lane; i < M; i += 32) {
+            sd[i] = i < m ? dd[b0 + i] : kInf;
+            si[i] = i < m ? ii[b0 + i] : kInvalid;
+        }
+        __syncwarp();
+        warp_sort_smem(sd, si, M, (int)lane);
+        const uint32_t na = sorted, nk = min(k, na + m);
+        float od[kOut];
+        uint32_t oi[kOut];
+#pragma unroll
+        for (int t = 0; t < kOut; ++t) {
+            const uint32_t o = lane + 32u * t;
+            if (o >= nk) break;
+            // co-rank: i entries of the prefix and o - i of the batch precede output o
+            uint32_t lo = o > m ? o - m : 0u, hi = min(o, na);
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (closer(dd[mid], ii[mid], sd[o - mid - 1], si[o - mid - 1])) lo = mid + 1;
+                else hi = mid;
+            }
+            const uint32_t j = o - lo;
+            const bool from_a = j >= m || (lo < na && closer(dd[lo], ii[lo], sd[j], si[j]));
+            od[t] = from_a ? dd[lo] : sd[j];
+            oi[t] = from_a ? ii[lo] : si[j];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kOut; ++t) {
+            const uint32_t o = lane + 32u * t;
+            if (o >= nk) break;
+            dd[o] = od[t];
+            ii[o] = oi[t];
+        }
+        __syncwarp();
+        sorted = nk;
+    }
+}
+
+// One packed update: accumulators of the query pair qq against row value b.  The
+// product is formed as fma(x, y, nz) with nz = (-0, -0) read from the kernel
+// arguments: x * y + (-0) is x * y rounded once (for every x * y, signed zeros
+// included), and ptxas cannot fold an addend it cannot see into the following add,
+// so the reference's two roundings stay (a plain mul.rn.f32x2 feeding add.rn.f32x2
+// is contracted into one FFMA2).  Three FP-pipe instructions per packed update, no
+// ALU-pipe masking.
+template <int METRIC>
+__device__ __forceinline__ void scan_step(unsigned long long& acc, unsigned long long qq, float b,
+                                          unsigned long long nz) {
+    unsigned long long tt;
+    if (METRIC == 0) {
+        const unsigned long long df = f2_sub(qq, f2_dup(b));
+        tt = f2_fma(df, df, nz);
+    } else {
+        tt = f2_fma(qq, f2_dup(b), nz);
+    }
+    acc = f2_add(acc, tt);
+}
+
 template <int METRIC>
 __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* qs = reinterpret_cast<unsigned long long*>(smem);          // [DC][QT]
-    float* bs = reinterpret_cast<float*>(smem + kScanDC * kScanQT * 8);              // [DC][BPitch]
-    float* cd = bs + kScanDC * kScanBPitch;                                          // [QT][P]
+    float* rs = reinterpret_cast<float*>(smem);                                      // [2][BT][RPitch]
+    float* qs = rs + 2 * kScanRowBuf;                                                // [2][DC][QT]
+    float* cd = qs + 2 * kScanQBuf;                                                  // [QT][P]
     uint32_t* ci = reinterpret_cast<uint32_t*>(cd + kScanQT * a.P);                 // [QT][P]
-    uint32_t* cnt = ci + kScanQT * a.P;                                              // [QT]
-    float* thr_d = reinterpret_cast<float*>(cnt + kScanQT);                          // [QT]
+    float* sd = reinterpret_cast<float*>(ci + kScanQT * a.P);                        // [warps][SortN]
+    uint32_t* si = reinterpret_cast<uint32_t*>(sd + kScanThreads / 32 * kScanSortN);  // [warps][SortN]
+    uint32_t* cnt = si + kScanThreads / 32 * kScanSortN;                             // [QT]
+    uint32_t* srt = cnt + kScanQT;                                                   // [QT] sorted prefix
+    float* thr_d = reinterpret_cast<float*>(srt + kScanQT);                          // [QT]
     uint32_t* thr_i = reinterpret_cast<uint32_t*>(thr_d + kScanQT);                 // [QT]
 
     const float kInf = __int_as_float(0x7f800000);
@@ -109,106 +194,121 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
     const uint32_t r_end = min(a.n, r_begin + a.rows_per_split);
     if (tid < kScanQT) {
         cnt[tid] = 0;
+        srt[tid] = 0;
         thr_d[tid] = kInf;
         thr_i[tid] = kInvalid;
     }
+    const unsigned long long nz = a.keep & 0x8000000080000000ull;  // (-0, -0), opaque
+    const uint32_t nchunks = (a.d + kScanDC - 1) / kScanDC;
+    const uint32_t ntiles = r_end > r_begin ? (r_end - r_begin + kScanBT - 1) / kScanBT : 0;
+    const uint32_t steps = ntiles * nchunks;
 
-    // chunk loader: base 128 rows x 32 dims = 1024 float4 (4 per thread), queries
-    // 32 x 32 = 256 float4 (1 per thread)
-    float4 rb[4], rq;
-    auto load_chunk = [&](uint32_t row0, uint32_t c0) {
+    // step s = (tile s / nchunks, chunk s % nchunks) -> buffer s & 1
+    // rows: 128 rows x 32 dims = 1024 x 16 B, 8 cp.async per thread (8 lanes per row)
+    // queries: 32 x 32 dims = 256 float4, 2 per thread, through registers (lane ->
+    // query, so the transposed stores are conflict-free)
+    float4 rq[2];
+    auto issue = [&](uint32_t s) {
+        const uint32_t row0 = r_begin + (s / nchunks) * kScanBT, c0 = (s % nchunks) * kScanDC;
+        float* rb = rs + (s & 1u) * kScanRowBuf;
 #pragma unroll
-        for (uint32_t t = 0; t < 4; ++t) {
+        for (uint32_t t = 0; t < 8; ++t) {
             const uint32_t f = tid + t * kScanThreads;
-            const uint32_t row = row0 + (f >> 3), dim = c0 + (f & 7u) * 4;
-            rb[t] = (row < r_end && dim < a.ld_b)
-                        ? __ldg(reinterpret_cast<const float4*>(a.base + (size_t)row * a.ld_b + dim))
+            const uint32_t r = f >> 3, dim = c0 + (f & 7u) * 4;
+            if (row0 + r < r_end && dim < a.ld_b)
+                cp_async16(rb + r * kScanRPitch + (f & 7u) * 4, a.base + (size_t)(row0 + r) * a.ld_b + dim);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+        for (uint32_t t = 0; t < 2; ++t) {
+            const uint32_t f = tid + t * kScanThreads;
+            const uint32_t q = q0 + (f & 31u), dim = c0 + (f >> 5) * 4;
+            rq[t] = (q < a.nq && dim < a.ld_q)
+                        ? __ldg(reinterpret_cast<const float4*>(a.queries + (size_t)q * a.ld_q + dim))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const uint32_t q = q0 + (tid >> 3), dim = c0 + (tid & 7u) * 4;
-        rq = (q < a.nq && dim < a.ld_q)
-                 ? __ldg(reinterpret_cast<const float4*>(a.queries + (size_t)q * a.ld_q + dim))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
     };
-    auto store_chunk = [&]() {
+    auto store_q = [&](uint32_t s) {
+        float* qb = qs + (s & 1u) * kScanQBuf;
 #pragma unroll
-        for (uint32_t t = 0; t < 4; ++t) {
+        for (uint32_t t = 0; t < 2; ++t) {
             const uint32_t f = tid + t * kScanThreads;
-            const uint32_t row = f >> 3, dim = (f & 7u) * 4;
-            bs[(dim + 0) * kScanBPitch + row] = rb[t].x;
-            bs[(dim + 1) * kScanBPitch + row] = rb[t].y;
-            bs[(dim + 2) * kScanBPitch + row] = rb[t].z;
-            bs[(dim + 3) * kScanBPitch + row] = rb[t].w;
+            const uint32_t q = f & 31u, dim = (f >> 5) * 4;
+            qb[(dim + 0) * kScanQT + q] = rq[t].x;
+            qb[(dim + 1) * kScanQT + q] = rq[t].y;
+            qb[(dim + 2) * kScanQT + q] = rq[t].z;
+            qb[(dim + 3) * kScanQT + q] = rq[t].w;
         }
-        const uint32_t q = tid >> 3, dim = (tid & 7u) * 4;
-        qs[(dim + 0) * kScanQT + q] = f2_dup(rq.x);
-        qs[(dim + 1) * kScanQT + q] = f2_dup(rq.y);
-        qs[(dim + 2) * kScanQT + q] = f2_dup(rq.z);
-        qs[(dim + 3) * kScanQT + q] = f2_dup(rq.w);
     };
 
-    for (uint32_t row0 = r_begin; row0 < r_end; row0 += kScanBT) {
-        // acc[2*qi + h*... ]: query qi (0..1) x row pair p (0..3):
-        //   p=0: rows 4tb+0,1  p=1: 4tb+2,3  p=2: 64+4tb+0,1  p=3: 64+4tb+2,3
-        unsigned long long acc[8];
+    // acc[2 * i + qp]: row tb + 16 i x queries (4tq + 2qp, 4tq + 2qp + 1)
+    unsigned long long acc[16];
+    if (steps > 0) {
+        issue(0);
+        store_q(0);
+    }
+    for (uint32_t s = 0; s < steps; ++s) {
+        const uint32_t c = s % nchunks;
+        const uint32_t row0 = r_begin + (s / nchunks) * kScanBT;
+        if (c == 0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0ull;
-        load_chunk(row0, 0);
-        for (uint32_t c0 = 0; c0 < a.d; c0 += kScanDC) {
-            __syncthreads();  // previous chunk fully consumed
-            store_chunk();
-            __syncthreads();
-            if (c0 + kScanDC < a.d) load_chunk(row0, c0 + kScanDC);  // in flight meanwhile
-            const uint32_t dims = min(kScanDC, a.d - c0);
-            const unsigned long long* qp = qs + 2 * tq;
-            const float* bp0 = bs + 4 * tb;
-            const float* bp1 = bs + 64 + 4 * tb;
-            auto step = [&](uint32_t t) {
-                const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qp + t * kScanQT);
-                const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(bp0 + t * kScanBPitch);
-                const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(bp1 + t * kScanBPitch);
-                const unsigned long long bv[4] = {b0.x, b0.y, b1.x, b1.y};
-                const unsigned long long qq[2] = {qv.x, qv.y};
+            for (int i = 0; i < 16; ++i) acc[i] = 0ull;
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // step s staged by all; step s - 1 consumed by all
+        if (s + 1 < steps) issue(s + 1);
+        const float* rb = rs + (s & 1u) * kScanRowBuf + tb * kScanRPitch;
+        const float* qb = qs + (s & 1u) * kScanQBuf + 4 * tq;
+        const uint32_t dims = min(kScanDC, a.d - c * kScanDC);
+        if (dims == kScanDC) {
+#pragma unroll 2
+            for (uint32_t j4 = 0; j4 < kScanDC; j4 += 4) {
+                float4 bv[8];
 #pragma unroll
-                for (int qi = 0; qi < 2; ++qi) {
+                for (int i = 0; i < 8; ++i)
+                    bv[i] = *reinterpret_cast<const float4*>(rb + i * 16 * kScanRPitch + j4);
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        unsigned long long tt;
-                        if (METRIC == 0) {
-                            const unsigned long long df = f2_sub(qq[qi], bv[p]);
-                            tt = f2_mul(df, df);
-                        } else {
-                            tt = f2_mul(qq[qi], bv[p]);
-                        }
-                        acc[qi * 4 + p] = f2_add(acc[qi * 4 + p], opaque(tt, a.keep));
+                for (int jj = 0; jj < 4; ++jj) {
+                    const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + (j4 + jj) * kScanQT);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float b = jj == 0 ? bv[i].x : jj == 1 ? bv[i].y : jj == 2 ? bv[i].z : bv[i].w;
+                        scan_step<METRIC>(acc[2 * i + 0], qv.x, b, nz);
+                        scan_step<METRIC>(acc[2 * i + 1], qv.y, b, nz);
                     }
                 }
-            };
-            if (dims == kScanDC) {
-#pragma unroll 8
-                for (uint32_t t = 0; t < kScanDC; ++t) step(t);
-            } else {
-                for (uint32_t t = 0; t < dims; ++t) step(t);
+            }
+        } else {
+            for (uint32_t j = 0; j < dims; ++j) {
+                const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + j * kScanQT);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float b = rb[i * 16 * kScanRPitch + j];
+                    scan_step<METRIC>(acc[2 * i + 0], qv.x, b, nz);
+                    scan_step<METRIC>(acc[2 * i + 1], qv.y, b, nz);
+                }
             }
         }
+        if (s + 1 < steps) store_q(s + 1);  // buffer (s + 1) & 1 was released at the barrier
+        if (c + 1 < nchunks) continue;
 
-        // ---- filter: append pairs closer than the query's current bound ----------
+        // ---- tile done: append pairs closer than the query's current bound ---------
 #pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-            const uint32_t ql = 2 * tq + qi;
-            const uint32_t q = q0 + ql;
-            if (q >= a.nq) continue;
-            const float td = thr_d[ql];
-            const uint32_t ti = thr_i[ql];
+        for (int qp = 0; qp < 2; ++qp) {
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t ql = 4 * tq + 2 * qp + h;
+                const uint32_t q = q0 + ql;
+                if (q >= a.nq) continue;
+                const float td = thr_d[ql];
+                const uint32_t ti = thr_i[ql];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t row = row0 + (p >> 1) * 64 + 4 * tb + (p & 1) * 2 + h;
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t row = row0 + tb + 16 * i;
                     if (row >= r_end) continue;
                     if (a.exclude_self && (uint64_t)row == a.self_base + q) continue;
-                    const float acc_v = h ? f2_hi(acc[qi * 4 + p]) : f2_lo(acc[qi * 4 + p]);
-                    const float dist = finish_exact<METRIC>(acc_v);
+                    const unsigned long long v = acc[2 * i + qp];
+                    const float dist = finish_exact<METRIC>(h ? f2_hi(v) : f2_lo(v));
                     if (closer(dist, row, td, ti)) {
                         const uint32_t pos = atomicAdd(&cnt[ql], 1u);
                         cd[ql * a.P + pos] = dist;
@@ -219,39 +319,35 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
         }
         __syncthreads();
         // ---- compact buffers that could overflow on the next tile ------------------
-        const bool last = row0 + kScanBT >= r_end;
+        const bool last = s + 1 == steps;
         for (uint32_t ql = warp; ql < kScanQT; ql += kScanThreads / 32) {
-            const uint32_t c = cnt[ql];
-            if (!last && c <= a.P - kScanBT) continue;
-            float* dd = cd + ql * a.P;
-            uint32_t* ii = ci + ql * a.P;
-            for (uint32_t i = c + lane; i < a.P; i += 32) {
-                dd[i] = kInf;
-                ii[i] = kInvalid;
-            }
-            __syncwarp();
-            warp_sort_smem(dd, ii, a.P, (int)lane);
-            const uint32_t kept = min(c, a.k);
+            const uint32_t cq = cnt[ql];
+            if (last ? cq == srt[ql] : cq <= a.P - kScanBT) continue;
+            scan_compact(cd + ql * a.P, ci + ql * a.P, srt[ql], cq, a.k, sd + warp * kScanSortN,
+                         si + warp * kScanSortN, lane);
+            const uint32_t kept = min(cq, a.k);
             if (lane == 0) {
                 cnt[ql] = kept;
+                srt[ql] = kept;
                 if (kept == a.k) {
-                    thr_d[ql] = dd[a.k - 1];
-                    thr_i[ql] = ii[a.k - 1];
+                    thr_d[ql] = cd[ql * a.P + a.k - 1];
+                    thr_i[ql] = ci[ql * a.P + a.k - 1];
                 }
             }
             __syncwarp();
         }
-        __syncthreads();
+        // the next step's barrier orders these updates before the next filter
     }
+    __syncthreads();
 
     // ---- write this split's top-k (sorted; padded with sentinels) -----------------
     for (uint32_t ql = warp; ql < kScanQT; ql += kScanThreads / 32) {
         const uint32_t q = q0 + ql;
         if (q >= a.nq) continue;
-        const uint32_t c = cnt[ql];  // sorted, <= k (every split ends with a compaction)
+        const uint32_t cq = cnt[ql];  // sorted, <= k (every split ends with a compaction)
         const size_t o = ((size_t)blockIdx.y * a.nq + q) * a.k;
         for (uint32_t i = lane; i < a.k; i += 32) {
-            const bool ok = r_end > r_begin && i < c;
+            const bool ok = r_end > r_begin && i < cq;
             a.out_ids[o + i] = ok ? ci[ql * a.P + i] : kInvalid;
             a.out_dists[o + i] = ok ? cd[ql * a.P + i] : kInf;
         }

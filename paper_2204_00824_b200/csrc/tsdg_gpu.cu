@@ -748,16 +748,8 @@ namespace {
 
 // ---- exact top-k scan (ground truth / brute-force k-NN graph) ----------------
 constexpr uint32_t kScanMaxK = 384;
-// Candidate buffer per query: the next power of 2 >= k + one tile of rows.
-uint32_t scan_buffer(uint32_t k) {
-    uint32_t P = 1;
-    while (P < k + kScanBT) P <<= 1;
-    return P;
-}
-size_t scan_smem(uint32_t P) {
-    return (size_t)kScanDC * kScanQT * 8 + (size_t)kScanDC * kScanBPitch * 4 +
-           (size_t)kScanQT * P * 8 + kScanQT * 12;
-}
+// Candidate buffer per query: k kept + one tile of appended rows.
+uint32_t scan_buffer(uint32_t k) { return round_up(k + kScanBT, 4); }
 
 void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const float* d_queries,
                        uint32_t nq, uint32_t ld_q, uint32_t d, uint32_t k, int metric,
@@ -785,7 +777,7 @@ void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const flo
     a.exclude_self = exclude_self;
     a.self_base = self_base;
     a.keep = ~0ull;
-    const size_t smem = scan_smem(a.P);
+    const size_t smem = scan_smem_bytes(a.P);
     void (*kern)(ScanArgs) = metric == 0 ? exact_scan_kernel<0>
                              : metric == 1 ? exact_scan_kernel<1> : exact_scan_kernel<2>;
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(exact_scan)");
