@@ -36,7 +36,9 @@
 namespace tsdg_dev {
 
 constexpr uint32_t kScanQT = 32;        // queries per CTA
-constexpr uint32_t kScanBT = 128;       // base rows per tile
+constexpr uint32_t kScanBT = 128;       // base rows per tile (64 with 3 CTAs per SM: same C2 time, C4 2% slower)
+constexpr int kScanRPT = kScanBT / 16;   // rows per thread (tb + 16 i)
+constexpr int kScanMinBlocks = kScanBT == 64 ? 3 : 2;  // CTAs per SM (shared memory)
 constexpr uint32_t kScanDC = 32;        // dims per chunk
 constexpr uint32_t kScanThreads = 128;
 constexpr uint32_t kScanRPitch = kScanDC + 4;  // floats per staged row (conflict-free LDS.128)
@@ -172,8 +174,17 @@ __device__ __forceinline__ void scan_step(unsigned long long& acc, unsigned long
     acc = f2_add(acc, tt);
 }
 
+// First half of scan_step for the sweep form: L2 leaves the difference (squared in
+// a second sweep), IP / cosine the finished product.
 template <int METRIC>
-__global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanArgs a) {
+__device__ __forceinline__ void scan_prod(unsigned long long& tt, unsigned long long qq, float b,
+                                          unsigned long long nz) {
+    if (METRIC == 0) tt = f2_sub(qq, f2_dup(b));
+    else tt = f2_fma(qq, f2_dup(b), nz);
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kernel(const ScanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* rs = reinterpret_cast<float*>(smem);                                      // [2][BT][RPitch]
     float* qs = rs + 2 * kScanRowBuf;                                                // [2][DC][QT]
@@ -212,7 +223,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
         const uint32_t row0 = r_begin + (s / nchunks) * kScanBT, c0 = (s % nchunks) * kScanDC;
         float* rb = rs + (s & 1u) * kScanRowBuf;
 #pragma unroll
-        for (uint32_t t = 0; t < 8; ++t) {
+        for (uint32_t t = 0; t < (uint32_t)kScanRPT; ++t) {
             const uint32_t f = tid + t * kScanThreads;
             const uint32_t r = f >> 3, dim = c0 + (f & 7u) * 4;
             if (row0 + r < r_end && dim < a.ld_b)
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
     };
 
     // acc[2 * i + qp]: row tb + 16 i x queries (4tq + 2qp, 4tq + 2qp + 1)
-    unsigned long long acc[16];
+    unsigned long long acc[2 * kScanRPT];
     if (steps > 0) {
         issue(0);
         store_q(0);
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
         const uint32_t row0 = r_begin + (s / nchunks) * kScanBT;
         if (c == 0) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0ull;
+            for (int i = 0; i < 2 * kScanRPT; ++i) acc[i] = 0ull;
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();  // step s staged by all; step s - 1 consumed by all
@@ -263,26 +274,36 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
         if (dims == kScanDC) {
 #pragma unroll 2
             for (uint32_t j4 = 0; j4 < kScanDC; j4 += 4) {
-                float4 bv[8];
+                float4 bv[kScanRPT];
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < kScanRPT; ++i)
                     bv[i] = *reinterpret_cast<const float4*>(rb + i * 16 * kScanRPitch + j4);
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + (j4 + jj) * kScanQT);
+                    // one dim in three sweeps over the 2 * RPT accumulators, so that
+                    // dependent instructions sit 2 * RPT apart (the per-accumulator
+                    // sub -> fma -> add chain otherwise stalls on fixed latencies)
+                    unsigned long long tt[2 * kScanRPT];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
+                    for (int i = 0; i < kScanRPT; ++i) {
                         const float b = jj == 0 ? bv[i].x : jj == 1 ? bv[i].y : jj == 2 ? bv[i].z : bv[i].w;
-                        scan_step<METRIC>(acc[2 * i + 0], qv.x, b, nz);
-                        scan_step<METRIC>(acc[2 * i + 1], qv.y, b, nz);
+                        scan_prod<METRIC>(tt[2 * i + 0], qv.x, b, nz);
+                        scan_prod<METRIC>(tt[2 * i + 1], qv.y, b, nz);
                     }
+                    if (METRIC == 0) {
+#pragma unroll
+                        for (int i = 0; i < 2 * kScanRPT; ++i) tt[i] = f2_fma(tt[i], tt[i], nz);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2 * kScanRPT; ++i) acc[i] = f2_add(acc[i], tt[i]);
                 }
             }
         } else {
             for (uint32_t j = 0; j < dims; ++j) {
                 const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + j * kScanQT);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < kScanRPT; ++i) {
                     const float b = rb[i * 16 * kScanRPitch + j];
                     scan_step<METRIC>(acc[2 * i + 0], qv.x, b, nz);
                     scan_step<METRIC>(acc[2 * i + 1], qv.y, b, nz);
@@ -303,7 +324,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) exact_scan_kernel(const ScanA
                 const float td = thr_d[ql];
                 const uint32_t ti = thr_i[ql];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < kScanRPT; ++i) {
                     const uint32_t row = row0 + tb + 16 * i;
                     if (row >= r_end) continue;
                     if (a.exclude_self && (uint64_t)row == a.self_base + q) continue;

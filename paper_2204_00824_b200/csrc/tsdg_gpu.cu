@@ -787,8 +787,9 @@ void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const flo
     // split the base rows so that the grid is >= ~4 waves; each split >= 8 tiles
     uint32_t S = std::max<uint32_t>(1, (4 * slots + qtiles - 1) / qtiles);
     S = std::min<uint32_t>(S, std::max<uint32_t>(1, n / (8 * kScanBT)));
-    S = std::min<uint32_t>(S, 64);
     if (env_int("TSDG_SCAN_SPLITS", 0) > 0) S = (uint32_t)env_int("TSDG_SCAN_SPLITS", 0);
+    // merge_splits_kernel follows one split list per lane
+    S = std::min<uint32_t>(S, 32);
     uint32_t rows = round_up((std::max<uint32_t>(n, 1) + S - 1) / S, kScanBT);
     S = std::max<uint32_t>(1, (n + rows - 1) / rows);
     a.rows_per_split = rows;

@@ -100,6 +100,23 @@ def test_gpu_brute_force_knn_bit_exact(scan_golden, name):
 
 
 @pytest.mark.gpu
+def test_gpu_scan_few_queries_max_splits():
+    """A handful of queries over a base long enough for the launcher's largest split
+    count (the merge follows at most 32 split lists, one per lane): same ids and
+    distance bits as the oracle, for small and large k."""
+    from paper_2204_00824_b200 import search
+    spec = {"kind": "lowlid", "n": 60000, "nq": 3, "d": 12, "latent": 6, "clusters": 10,
+            "spread": 0.25, "seed": 21, "noise": 0.01}
+    b, q = datasets.generate(spec)
+    orc = O.Oracle()
+    for k in (10, 300):
+        wi, wd = orc.exact_topk(b, q, k)
+        r = search.ground_truth(b, q, k)
+        np.testing.assert_array_equal(r.ids, wi)
+        np.testing.assert_array_equal(_bits(r.dists), _bits(wd))
+
+
+@pytest.mark.gpu
 def test_gpu_scan_splits_and_index_form(scan_golden):
     """Many queries (several base splits + the device merge) and the index-resident
     form agree with the oracle; larger k exercises the 512-entry candidate buffer."""

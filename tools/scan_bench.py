@@ -6,8 +6,11 @@
   * brute-force k-NN graph (k=100) of the C1 base (100K x 128).
 
 Prints one JSON line per case: seconds (CUDA events around the device call), pair
-distances per second and the fp32-pipe roofline (3 flops per pair-dim: sub, mul, add
-— no FMA, the reference's rounding)."""
+distances per second and the fp32-pipe roofline: 3 ops per pair-dim (sub, mul, add —
+no FMA, the reference's rounding) against the packed-pipe rate measured by
+tools/micro/fp2_pipes.cu (FADD2 / FMUL2: 127.7 lane-ops per SM per cycle, i.e. one
+packed instruction per two cycles per SMSP; the kernel's own step — SUB2, FFMA2 with
+a -0 addend, ADD2 — at best 112 in that probe)."""
 import json
 import os
 import sys
@@ -22,7 +25,8 @@ import torch  # noqa: E402
 
 from paper_2204_00824_b200 import _native, datasets  # noqa: E402
 
-FP32_PEAK = 148 * 128 * 2 * 1.965e9  # packed f32x2: 2 flops / lane / cycle (~74.4 TFLOP/s)
+FP2_PEAK = 148 * 128 * 1.965e9  # fp32 lane-ops/s of the packed pipe (37.2 T), measured rate
+STEP_CAP = 148 * 112 * 1.965e9  # the scan step's own best in the probe (32.6 T)
 
 
 def timed(fn, reps=2):
@@ -72,7 +76,8 @@ def gt_case(name, k=100):
         sec = timed(call)
         flops = 3.0 * nq * n * d
         out.update({"device_s": sec, "pairs_per_s": nq * n / sec,
-                    "fp32_TFLOPs": flops / sec / 1e12, "fp32_frac": flops / sec / FP32_PEAK})
+                    "fp32_Tops": flops / sec / 1e12, "fp2_pipe_frac": flops / sec / FP2_PEAK,
+                    "frac_of_probe_step": flops / sec / STEP_CAP})
     return out
 
 
@@ -98,7 +103,7 @@ def knn_case(name="c1_lowlid_100k", k=100):
         ok &= bool(np.allclose(got, want, rtol=1e-5, atol=1e-6))
     flops = 3.0 * n * n * d
     return {"case": f"brute_force_knn {name}", "n": n, "d": d, "k": kg.k,
-            "host_call_s": sec, "fp32_TFLOPs_incl_copies": flops / sec / 1e12,
+            "host_call_s": sec, "fp32_Tops_incl_copies": flops / sec / 1e12,
             "float64_spot_check_50_nodes": ok}
 
 
