@@ -57,6 +57,9 @@ struct GcArgs {
                             // evaluated node (the next hop's u is one of them)
     uint32_t npow2;      // pool size for the in-cluster merge
     uint32_t dch, slots;
+    uint32_t stage;       // host: StageKind the kernel was chosen for
+    const void* tmap;     // kStageG4: tensor map of vec (global memory)
+    uint32_t gpitch;      // kStageG4: floats between 4-slot groups
     uint32_t off_query, off_stage, off_bar, off_ctl, off_list, off_pool, off_rowid, off_pos;
 };
 
@@ -148,7 +151,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sq = m.sq;
     GcCtl* ctl = m.ctl;
-    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots, 0, a.tmap, a.gpitch};
     const float kInf = __int_as_float(0x7f800000);
 
     TR_MARK(0)
@@ -523,10 +526,11 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     const GcSmem m = gc_smem(a, smem_raw);
     WarpStage w;
     w.sq = m.sq;
-    w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) + (size_t)warp * a.slots * (a.dch + 4);
+    w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) +
+              (size_t)warp * (STAGE == kStageG4 ? a.slots / 4 * a.gpitch : a.slots * (a.dch + 4));
     w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
     w.parity = 0;
-    w.rowid = STAGE == kStageLdgsts ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;
+    w.rowid = STAGE != kStageTma ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;
     if (lane == 0) mbar_init(w.bar, 1);
     GcOut o;
     o.ids = a.out_ids ? a.out_ids + (size_t)q * a.k : nullptr;

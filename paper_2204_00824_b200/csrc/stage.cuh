@@ -12,6 +12,14 @@
 // warp = more resident warps, at the cost of more gather rounds).
 //   kStageTma     one cp.async.bulk (TMA, UBLKCP) per row, completion counted on
 //                 the warp's mbarrier.
+//   kStageG4      TMA tile::gather4 tensor copies: four rows (any row ids) per
+//                 instruction through a 2-D tensor map of the vectors (box {dch+4, 1};
+//                 the 4 columns past a 128-float row are out of bounds and zero
+//                 filled, which gives the padded slot pitch).  A tensor copy needs a
+//                 128-byte aligned destination, so the slots sit in groups of 4 at a
+//                 gpitch = round_up(4 (dch+4), 32) float stride.  32 rows: 8 issues
+//                 instead of 32 (tools/micro/gather4_probe.cu: 1128 vs 2251 cycles
+//                 from issue to completion, L2-warm).  Rows of at most 128 floats.
 // Distances:
 //   exact  the reference's order (vectors.hpp:36-49): acc = ((0+t0)+t1)+..., with
 //          t_i = (q_i - r_i)^2 rounded separately — packed FADD2/FMUL2 (f32x2, one
@@ -25,14 +33,14 @@
 
 namespace tsdg_dev {
 
-enum StageKind { kStageLdgsts = 0, kStageTma = 1 };
+enum StageKind { kStageLdgsts = 0, kStageTma = 1, kStageG4 = 2 };
 
 struct WarpStage {
     float* sq;      // query, ld floats (zero padded)
     float* stage;   // 32 x (dch + 4)
     uint64_t* bar;  // TMA path
     uint32_t parity;
-    uint32_t* rowid;  // LDGSTS path: row id per slot (32), or nullptr (then __fns)
+    uint32_t* rowid;  // LDGSTS / gather4 paths: row id per slot (32), or nullptr (then __fns)
 };
 
 struct Geom {
@@ -40,7 +48,43 @@ struct Geom {
     uint32_t ld, d, dch;
     uint32_t slots;  // shared-memory row slots per warp (1..32)
     uint32_t pitch;  // floats between slots (0: dch + 4, an odd number of 16-byte units)
+    const void* tmap;  // kStageG4: the vectors' tensor map (global memory), else unused
+    uint32_t gpitch;   // kStageG4: floats between 4-slot groups
 };
+
+// Slot s of a warp's staging slab.
+template <int STAGE>
+__device__ __forceinline__ float* slot_ptr(float* stage, const Geom& g, uint32_t pitch, uint32_t s) {
+    return STAGE == kStageG4 ? stage + (s >> 2) * g.gpitch + (s & 3u) * pitch : stage + s * pitch;
+}
+
+// tile::gather4: rows r0..r3 (columns c0 .. c0 + box) of the tensor map into four
+// consecutive boxes at dst (128-byte aligned), completion counted on bar.
+__device__ __forceinline__ void bulk_gather4(void* dst, const void* tmap, uint32_t c0, uint32_t r0,
+                                             uint32_t r1, uint32_t r2, uint32_t r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_addr(dst)),
+        "l"(tmap), "r"(smem_addr(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
+// Issue the gather4 copies of `cnt` rows whose ids are in rowid[0, cnt) (slot r <- row
+// rowid[r]); a partial last group repeats its first row.  Lane 0 arms the barrier.
+__device__ __forceinline__ void g4_issue(WarpStage& w, const Geom& g, uint32_t cnt, int lane) {
+    const uint32_t pitch = g.dch + 4;
+    const uint32_t ng = (cnt + 3) >> 2;
+    if (lane == 0) mbar_arrive_expect_tx(w.bar, ng * 16u * pitch);
+    __syncwarp();
+    if ((uint32_t)lane < ng) {
+        const uint32_t b = 4u * (uint32_t)lane;
+        const uint32_t r0 = w.rowid[b];
+        const uint32_t r1 = b + 1 < cnt ? w.rowid[b + 1] : r0;
+        const uint32_t r2 = b + 2 < cnt ? w.rowid[b + 2] : r0;
+        const uint32_t r3 = b + 3 < cnt ? w.rowid[b + 3] : r0;
+        bulk_gather4(w.stage + (size_t)lane * g.gpitch, g.tmap, 0, r0, r1, r2, r3, w.bar);
+    }
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
@@ -169,12 +213,20 @@ __device__ __forceinline__ float gather_eval(WarpStage& w, const Geom& g, bool n
         const uint32_t cslot = split ? ((uint32_t)lane & 15u) : (uint32_t)lane;
         const bool half = split && lane >= 16;
         const bool computes = cslot < nr;
-        const float* srow = w.stage + cslot * pitch;  // slot reduced by this lane
+        const float* srow = slot_ptr<STAGE>(w.stage, g, pitch, cslot);  // slot reduced by this lane
         float acc = 0.0f;
         unsigned long long acc2 = 0ull;
         for (uint32_t c0 = 0; c0 < g.ld; c0 += g.dch) {
             const uint32_t cw = min(g.dch, g.ld - c0);  // floats this round, multiple of 4
-            if (STAGE == kStageTma) {
+            if (STAGE == kStageG4) {  // whole rows (ld <= dch): one chunk
+                __syncwarp();  // the previous round's readers of rowid / the slots are done
+                if (mine_round) w.rowid[slot] = e;
+                fence_proxy_async_smem();
+                __syncwarp();
+                g4_issue(w, g, nr, lane);
+                mbar_wait(w.bar, w.parity);
+                w.parity ^= 1u;
+            } else if (STAGE == kStageTma) {
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_expect_tx(w.bar, nr * cw * 4u);
@@ -312,10 +364,22 @@ __device__ __forceinline__ void gather_issue_ldgsts(WarpStage& w, const Geom& g,
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// gather4 form of gather_issue (rows of at most dch floats, w.rowid set).
+__device__ __forceinline__ void gather_issue_g4(WarpStage& w, const Geom& g, bool need, uint32_t e,
+                                                int lane) {
+    const unsigned nm = __ballot_sync(kFull, need);
+    if (nm == 0) return;
+    __syncwarp();  // the slots' previous rows and rowid have been consumed
+    if (need) w.rowid[__popc(nm & ((1u << lane) - 1u))] = e;
+    fence_proxy_async_smem();
+    __syncwarp();
+    g4_issue(w, g, __popc(nm), lane);
+}
 template <int STAGE>
 __device__ __forceinline__ void gather_issue_s(WarpStage& w, const Geom& g, bool need, uint32_t e,
                                                int lane) {
     if (STAGE == kStageTma) gather_issue(w, g, need, e, lane);
+    else if (STAGE == kStageG4) gather_issue_g4(w, g, need, e, lane);
     else gather_issue_ldgsts(w, g, need, e, lane);
 }
 
@@ -327,7 +391,7 @@ __device__ __forceinline__ float gather_complete(WarpStage& w, const Geom& g, bo
     const uint32_t pitch = g.pitch ? g.pitch : g.dch + 4;
     const uint32_t cnt = __popc(nm);
     const uint32_t rank = __popc(nm & ((1u << lane) - 1u));
-    if (STAGE == kStageTma) {
+    if (STAGE != kStageLdgsts) {
         mbar_wait(w.bar, w.parity);
         w.parity ^= 1u;
     } else {
@@ -336,7 +400,7 @@ __device__ __forceinline__ float gather_complete(WarpStage& w, const Geom& g, bo
     }
     float dist = kInf;
     if ((uint32_t)lane < cnt) {  // lane r reduces slot r, in the reference's order
-        const float* srow = w.stage + lane * pitch;
+        const float* srow = slot_ptr<STAGE>(w.stage, g, pitch, (uint32_t)lane);
         float acc = 0.0f;
         unsigned long long acc2 = 0ull;
         const uint32_t quads = g.d >> 2;

@@ -4,6 +4,7 @@
 // deg_cut tables), validates parameters exactly like the reference front ends
 // (bestfirst_search.cpp:112-150, greedy_search.cpp:74-127), sizes the
 // persistent kernels for occupancy on the B200's 148 SMs and launches them.
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -154,6 +155,11 @@ struct tsdg_gpu_index {
     // grow-only device scratch for the host-pointer entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
+    // 2-D tensor map of the vectors for TMA tile::gather4 (greedy kernels), made on
+    // first use; device copy (64-byte aligned) or nullptr when not encodable
+    void* tmap = nullptr;
+    uint32_t tmap_box = 0;
+    bool tmap_tried = false;
 };
 
 namespace {
@@ -574,11 +580,51 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     cuda_check(cudaGetLastError(), "greedy_walk_kernel launch");
 }
 
+// Tensor map of the vectors for tile::gather4 row gathers: 2-D {ld, n} fp32, row
+// stride ld * 4 bytes, box {box, 1} (box = the staging pitch dch + 4: the columns past
+// ld are out of bounds and arrive as zeros).  Encoded once per index through the
+// driver entry point (no libcuda link); nullptr when the driver rejects it (the
+// kernels then stage with one bulk copy per row).  Caller holds idx->mu.
+const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
+    if (idx->tmap_tried) return idx->tmap_box == box ? idx->tmap : nullptr;
+    idx->tmap_tried = true;
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+    static Encode enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        (void)cudaGetLastError();
+        return reinterpret_cast<Encode>(fn);
+    }();
+    if (!enc || box > 256 || (box * 4) % 16 || idx->n == 0) return nullptr;
+    alignas(64) CUtensorMap tm;
+    const cuuint64_t gdim[2] = {idx->ld, idx->n};
+    const cuuint64_t gstride[1] = {(cuuint64_t)idx->ld * 4};
+    const cuuint32_t bdim[2] = {box, 1};
+    const cuuint32_t estride[2] = {1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, idx->vec, gdim, gstride, bdim, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return nullptr;
+    void* dev = nullptr;
+    cuda_check(cudaMalloc(&dev, sizeof(CUtensorMap)), "cudaMalloc(tensor map)");
+    cuda_check(cudaMemcpyAsync(dev, &tm, sizeof(CUtensorMap), cudaMemcpyHostToDevice, st), "H2D tensor map");
+    cuda_check(cudaStreamSynchronize(st), "tensor map upload");
+    idx->tmap = dev;
+    idx->tmap_box = box;
+    return dev;
+}
+
 // CTA-per-walk / cluster-per-query greedy (greedy_cluster.cuh).  Returns false when
 // the cluster launch is not possible (then the caller merges walks itself).
 // GcArgs + shared-memory carve of the CTA-per-walk kernels.
 size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* p,
-                    bool cluster, cudaStream_t st) {
+                    bool cluster, cudaStream_t st, uint32_t stage_req = kStageG4) {
     a.vec = idx->vec;
     a.adj = idx->adj;
     a.degcut = get_degcut(idx, p->lambda_cut, st);
@@ -599,16 +645,37 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     while (a.npow2 < p->t0 * 32) a.npow2 <<= 1;
     a.dch = staging_dims(idx->ld);
     a.slots = 32;
+    // row staging (TSDG_GC_STAGE=g4|tma|ldgsts): tile::gather4 tensor copies by
+    // default when the rows fit one staging round (ld <= dch) and the tensor map
+    // encodes; else one bulk copy per row
+    a.stage = kStageTma;
+    a.tmap = nullptr;
+    if (env_is("TSDG_GC_STAGE", "ldgsts")) {
+        a.stage = kStageLdgsts;
+    } else if (stage_req == kStageG4 && !env_is("TSDG_GC_STAGE", "tma") && idx->ld <= a.dch) {
+        a.tmap = vectors_tmap(idx, a.dch + 4, st);
+        if (a.tmap) a.stage = kStageG4;
+    }
+    a.gpitch = round_up(4 * (a.dch + 4), 32);
+    const uint32_t warp_stage = a.stage == kStageG4 ? a.slots / 4 * a.gpitch : a.slots * (a.dch + 4);
     Carve c;
     a.off_bar = c.take(8 * kGcWarps, 8);
     a.off_ctl = c.take(sizeof(GcCtl));
     a.off_list = c.take(32 * 8);
     a.off_query = c.take(a.ld * 4);
     a.off_pos = c.take((size_t)idx->R * 8);
-    a.off_stage = c.take(kGcWarps * a.slots * (a.dch + 4) * 4, 128);
+    a.off_stage = c.take(kGcWarps * warp_stage * 4, 128);
     a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 + 2 * a.t0 * 4 : 0);
     a.off_rowid = c.take(kGcWarps * 32 * 4);
     return round_up(c.total, 128);
+}
+
+template <int M>
+void (*pick_gc(bool fast, uint32_t stage))(GcArgs) {
+    if (stage == kStageG4) return fast ? greedy_cta_kernel<M, true, kStageG4> : greedy_cta_kernel<M, false, kStageG4>;
+    if (stage == kStageLdgsts)
+        return fast ? greedy_cta_kernel<M, true, kStageLdgsts> : greedy_cta_kernel<M, false, kStageLdgsts>;
+    return fast ? greedy_cta_kernel<M, true, kStageTma> : greedy_cta_kernel<M, false, kStageTma>;
 }
 
 bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint32_t k,
@@ -616,7 +683,22 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
                        uint32_t* d_ids, float* d_dists, uint32_t* d_counts,
                        tsdg_query_stats* d_stats, WalkBuffers* wb, cudaStream_t st) {
     GcArgs a{};
-    const size_t smem = fill_gc_args(a, idx, k, p, wb == nullptr, st);
+    size_t smem = fill_gc_args(a, idx, k, p, wb == nullptr, st);
+    if (a.stage == kStageG4 && !env_is("TSDG_GC_STAGE", "g4")) {
+        // the gather4 slab is ~3% larger (128-byte aligned 4-slot groups): when that
+        // costs a resident CTA per SM and the grid needs it, stage per row instead
+        // (C2, t0=10, batch 64: 117 vs 94 us)
+        GcArgs b{};
+        const size_t smem_t = fill_gc_args(b, idx, k, p, wb == nullptr, st, kStageTma);
+        int smem_sm = 0, resv = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, idx->device);
+        cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, idx->device);
+        const uint64_t per_g4 = (uint64_t)smem_sm / (smem + resv), per_t = (uint64_t)smem_sm / (smem_t + resv);
+        if (per_g4 < per_t && (uint64_t)nq * p->t0 > per_g4 * (uint64_t)idx->sm_count) {
+            a = b;
+            smem = smem_t;
+        }
+    }
     a.queries = d_queries;
     a.nq = nq;
     a.walk_states = d_states;
@@ -632,19 +714,13 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
     }
     using GcKernel = void (*)(GcArgs);
     GcKernel kern;
-    // row staging: TMA bulk copies (one per row) or LDGSTS (one coalesced 512 B row per
-    // warp instruction); TSDG_GC_STAGE selects.  Both pipelined across hops; C2 batch 1,
-    // t0=10: TMA 51 us, LDGSTS 59 us (its 32 cp.async per lane issue slower)
-    const bool ldg = env_is("TSDG_GC_STAGE", "ldgsts");
-    if (idx->metric == 0)
-        kern = fast ? (ldg ? greedy_cta_kernel<0, true, kStageLdgsts> : greedy_cta_kernel<0, true, kStageTma>)
-                    : (ldg ? greedy_cta_kernel<0, false, kStageLdgsts> : greedy_cta_kernel<0, false, kStageTma>);
-    else if (idx->metric == 1)
-        kern = fast ? (ldg ? greedy_cta_kernel<1, true, kStageLdgsts> : greedy_cta_kernel<1, true, kStageTma>)
-                    : (ldg ? greedy_cta_kernel<1, false, kStageLdgsts> : greedy_cta_kernel<1, false, kStageTma>);
-    else
-        kern = fast ? (ldg ? greedy_cta_kernel<2, true, kStageLdgsts> : greedy_cta_kernel<2, true, kStageTma>)
-                    : (ldg ? greedy_cta_kernel<2, false, kStageLdgsts> : greedy_cta_kernel<2, false, kStageTma>);
+    // row staging (fill_gc_args): gather4 tensor copies, TMA bulk copies (one per row)
+    // or LDGSTS (one coalesced 512 B row per warp instruction).  All pipelined across
+    // hops; C2 batch 1, t0=10: TMA 51 us, LDGSTS 59 us (its 32 cp.async per lane
+    // issue slower)
+    if (idx->metric == 0) kern = pick_gc<0>(fast, a.stage);
+    else if (idx->metric == 1) kern = pick_gc<1>(fast, a.stage);
+    else kern = pick_gc<2>(fast, a.stage);
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(greedy_cta)");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nq * p->t0);
@@ -1154,6 +1230,7 @@ void free_index(tsdg_gpu_index* idx) {
     if (idx->stream2) cudaStreamSynchronize(idx->stream2);
     for (auto& kv : idx->degcut) cudaFree(kv.second);
     if (idx->scratch) cudaFree(idx->scratch);
+    if (idx->tmap) cudaFree(idx->tmap);
     cudaFree(idx->vec);
     cudaFree(idx->adj);
     cudaFree(idx->lam);

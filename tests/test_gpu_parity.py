@@ -346,12 +346,15 @@ def test_greedy_kernels_bit_exact(orc, fixtures, index, golden, golden_meta, mon
 @pytest.mark.parametrize("merge_warp,early,stage,extra", [
     ("0", "0", "tma", {}), ("0", "1", "ldgsts", {}), ("1", "0", "tma", {}), ("1", "1", "tma", {}),
     ("1", "1", "ldgsts", {}), ("1", "0", "ldgsts", {}),
-    ("1", "1", "tma", {"TSDG_GC_SLICE": "16"}), ("1", "1", "tma", {"TSDG_GC_ADJ_PREFETCH": "1"})])
+    ("1", "1", "tma", {"TSDG_GC_SLICE": "16"}), ("1", "1", "tma", {"TSDG_GC_ADJ_PREFETCH": "1"}),
+    ("0", "0", "g4", {}), ("1", "0", "g4", {}), ("1", "1", "g4", {}),
+    ("1", "1", "g4", {"TSDG_GC_SLICE": "16"})])
 def test_greedy_cluster_kernel_variants_bit_exact(orc, fixtures, index, golden, golden_meta, monkeypatch,
                                                   merge_warp, early, stage, extra):
     """The greedy cluster kernel's internal variants — warp 0 merging while warps 1-3
-    gather (TSDG_GC_MERGE_WARP), the early next-node pick (TSDG_GC_EARLY), TMA or
-    cp.async row staging (TSDG_GC_STAGE) — all reproduce the reference."""
+    gather (TSDG_GC_MERGE_WARP), the early next-node pick (TSDG_GC_EARLY), row
+    staging by TMA bulk copies, TMA tile::gather4 tensor copies or cp.async
+    (TSDG_GC_STAGE) — all reproduce the reference."""
     monkeypatch.setenv("TSDG_GREEDY", "cta")
     monkeypatch.setenv("TSDG_GC_MERGE_WARP", merge_warp)
     monkeypatch.setenv("TSDG_GC_EARLY", early)
