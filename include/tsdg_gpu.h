@@ -31,10 +31,12 @@
  *   TSDG_FAST_PAIR=0|1      force the single / paired (two warps per query) fast
  *                           kernel (default: paired below one query per CTA slot)
  *   TSDG_FAST_VARIANT, TSDG_FAST_PREFETCH   fast-kernel tuning variants (bf_fast.cu)
- *   TSDG_STAGE=ldgsts, TSDG_SLOTS, TSDG_BF_WARPS, TSDG_PREFETCH, TSDG_BATCH_MIN
- *                           staged best-first kernel: staging path / slots / warps
+ *   TSDG_STAGE=g4|tma|ldgsts, TSDG_SLOTS, TSDG_BF_WARPS, TSDG_PREFETCH, TSDG_BATCH_MIN
+ *                           staged best-first kernel: staging path (default: TMA
+ *                           gather4 tensor copies in deterministic mode for rows of
+ *                           <= 128 floats, else one bulk copy per row) / slots / warps
  *   TSDG_GREEDY=cta|warp, TSDG_GREEDY_CTA_MAX_WALKS   greedy kernel routing
- *   TSDG_GC_STAGE=ldgsts, TSDG_GC_MERGE_WARP, TSDG_GC_SLICE, TSDG_GC_ADJ_PREFETCH,
+ *   TSDG_GC_STAGE=g4|tma|ldgsts, TSDG_GC_MERGE_WARP, TSDG_GC_SLICE, TSDG_GC_ADJ_PREFETCH,
  *   TSDG_GR_WARPS           greedy kernels' staging / warp roles
  *   TSDG_SCAN_SPLITS        exact-scan base splits
  *   TSDG_DEBUG_PATH=1, TSDG_LOAD_TRACE=1   diagnostics on stderr

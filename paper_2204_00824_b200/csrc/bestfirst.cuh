@@ -62,6 +62,8 @@ struct BfArgs {
     uint32_t warp_smem, off_query, off_stage, off_cid, off_cdist, off_csize, off_vid,
         off_vsize, off_voldest, off_rid, off_rdist, off_bar, off_rowid;
     uint32_t off_lst, off_dl;  // bf_fast_kernel: needed-row ids / distances (64 + pad)
+    const void* tmap;          // kStageG4: tensor map of vec (global memory)
+    uint32_t gpitch;           // kStageG4: floats between 4-slot groups
 };
 
 struct BfWarp {
@@ -399,11 +401,11 @@ __global__ void __launch_bounds__(kBfWarps * 32, TSDG_BF_MIN_BLOCKS) bf_kernel(c
     w.voldest = reinterpret_cast<uint32_t*>(ws + a.off_voldest);
     w.rid = reinterpret_cast<uint32_t*>(ws + a.off_rid);
     w.rdist = reinterpret_cast<float*>(ws + a.off_rdist);
-    if (STAGE == kStageTma) {
+    if (STAGE != kStageLdgsts) {
         if (lane == 0) mbar_init(w.st.bar, 1);
         __syncwarp();
     }
-    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots, 0};
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots, 0, a.tmap, a.gpitch};
     const float kInf = __int_as_float(0x7f800000);
     const bool pf_rows = (a.prefetch & 1u) != 0;
     const bool pf_adj = (a.prefetch & 2u) != 0;

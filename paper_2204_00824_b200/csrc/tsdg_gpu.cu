@@ -261,7 +261,8 @@ void fill_bf_layout(BfArgs& a) {
     Carve c;
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
+    a.gpitch = round_up(4 * (a.dch + 4), 32);
+    a.off_stage = c.take(a.tmap ? a.slots / 4 * a.gpitch * 4 : a.slots * (a.dch + 4) * 4, 128);
     a.off_cid = c.take((a.m + 1) * kSegPitch * 4);    // + one scratch row (batched admission)
     a.off_cdist = c.take((a.m + 1) * kSegPitch * 4);
     a.off_csize = c.take(a.m * 4);
@@ -294,14 +295,17 @@ bool env_is(const char* name, const char* val) {
 using BfKernel = void (*)(BfArgs);
 
 template <int METRIC, bool FAST>
-BfKernel pick_bf(bool tma, bool kreg) {
-    if (tma) return kreg ? bf_kernel<METRIC, FAST, kStageTma, true> : bf_kernel<METRIC, FAST, kStageTma, false>;
+BfKernel pick_bf(int stage, bool kreg) {
+    if (stage == kStageG4 && !FAST)  // gather4 staging: deterministic mode, whole rows
+        return kreg ? bf_kernel<METRIC, false, kStageG4, true> : bf_kernel<METRIC, false, kStageG4, false>;
+    if (stage != kStageLdgsts)
+        return kreg ? bf_kernel<METRIC, FAST, kStageTma, true> : bf_kernel<METRIC, FAST, kStageTma, false>;
     return kreg ? bf_kernel<METRIC, FAST, kStageLdgsts, true> : bf_kernel<METRIC, FAST, kStageLdgsts, false>;
 }
-BfKernel pick_bf(int metric, bool fast, bool tma, bool kreg) {
-    if (metric == 0) return fast ? pick_bf<0, true>(tma, kreg) : pick_bf<0, false>(tma, kreg);
-    if (metric == 1) return fast ? pick_bf<1, true>(tma, kreg) : pick_bf<1, false>(tma, kreg);
-    return fast ? pick_bf<2, true>(tma, kreg) : pick_bf<2, false>(tma, kreg);
+BfKernel pick_bf(int metric, bool fast, int stage, bool kreg) {
+    if (metric == 0) return fast ? pick_bf<0, true>(stage, kreg) : pick_bf<0, false>(stage, kreg);
+    if (metric == 1) return fast ? pick_bf<1, true>(stage, kreg) : pick_bf<1, false>(stage, kreg);
+    return fast ? pick_bf<2, true>(stage, kreg) : pick_bf<2, false>(stage, kreg);
 }
 
 // bf_fast_kernel per-warp carve: query (generic path), C and V in sentinel form
@@ -410,6 +414,8 @@ void launch_unbounded(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
     if (h_over) fail(TSDG_ERUNTIME, "bestfirst_search(unbounded): arena capacity exceeded");
 }
 
+const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st);
+
 void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint64_t qbase,
                       const tsdg_bf_params* p, int mode, uint32_t* d_ids, float* d_dists,
                       uint32_t* d_counts, tsdg_query_stats* d_stats, cudaStream_t st) {
@@ -483,11 +489,21 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         cuda_check(cudaGetLastError(), "bf_fast_kernel launch");
         return;
     }
+    // row staging (TSDG_STAGE=g4|tma|ldgsts): deterministic mode with whole rows
+    // (ld <= dch) and slots in groups of 4 uses gather4 tensor copies (C2 bench point:
+    // 1.100 vs 1.147 ms, identical results; tools/det_stage.py); else one bulk copy
+    // per row
+    int stage = env_is("TSDG_STAGE", "ldgsts") ? kStageLdgsts : kStageTma;
+    a.tmap = nullptr;
+    if (stage == kStageTma && !env_is("TSDG_STAGE", "tma") && mode != TSDG_MODE_FAST && idx->ld <= a.dch &&
+        a.slots % 4 == 0) {
+        a.tmap = vectors_tmap(idx, a.dch + 4, st);
+        if (a.tmap) stage = kStageG4;
+    }
     fill_bf_layout(a);
     const int wpc = std::max(1, std::min(kBfWarps, env_int("TSDG_BF_WARPS", 1)));
     const size_t smem = (size_t)a.warp_smem * wpc;
-    const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST,
-                                  !env_is("TSDG_STAGE", "ldgsts"), a.k <= 31);
+    const BfKernel kern = pick_bf(idx->metric, mode == TSDG_MODE_FAST, stage, a.k <= 31);
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf)");
     const int grid = grid_for(kern, wpc * 32, smem, idx->sm_count, nq, wpc);
     kern<<<grid, wpc * 32, smem, st>>>(a);
