@@ -41,7 +41,9 @@ struct GrArgs {
     uint32_t* work_counter;
     uint32_t work_base;     // counter value at launch (tsdg_gpu.cu next_counter)
     uint32_t dch, slots;
-    uint32_t warp_smem, off_query, off_stage, off_bar;
+    uint32_t warp_smem, off_query, off_stage, off_bar, off_rowid;
+    const void* tmap;   // kStageG4: tensor map of vec (global memory)
+    uint32_t gpitch;    // kStageG4: floats between 4-slot groups
 };
 
 // merge_halves (rank_list.cpp:20-49).  (rd, ri): R_ij slot `lane` (sorted);
@@ -109,9 +111,9 @@ __global__ void __launch_bounds__(kGrWarps * 32) greedy_walk_kernel(const GrArgs
     w.stage = reinterpret_cast<float*>(ws + a.off_stage);
     w.bar = reinterpret_cast<uint64_t*>(ws + a.off_bar);
     w.parity = 0;
-    w.rowid = nullptr;
-    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots};
-    if (STAGE == kStageTma) {
+    w.rowid = STAGE == kStageG4 ? reinterpret_cast<uint32_t*>(ws + a.off_rowid) : nullptr;
+    const Geom g{a.vec, a.ld, a.d, a.dch, a.slots, 0, a.tmap, a.gpitch};
+    if (STAGE != kStageLdgsts) {
         if (lane == 0) mbar_init(w.bar, 1);
         __syncwarp();
     }

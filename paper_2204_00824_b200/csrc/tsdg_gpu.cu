@@ -571,17 +571,26 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     a.work_base = tk.base;
     a.dch = staging_dims(idx->ld);
     a.slots = 32;
+    // row staging: gather4 tensor copies for L2 rows of <= dch floats (C2, t0=10,
+    // batch 256 / 1024 / 4096: 162 / 388 / 1304 vs 180 / 430 / 1437 us with one bulk
+    // copy per row, bit-exact); TSDG_GR_STAGE=tma forces per-row copies
+    const bool g4 = !env_is("TSDG_GR_STAGE", "tma") && idx->ld <= a.dch && idx->metric == 0 &&
+                    !env_is("TSDG_STAGE", "ldgsts") && (a.tmap = vectors_tmap(idx, a.dch + 4, st)) != nullptr;
+    a.gpitch = round_up(4 * (a.dch + 4), 32);
     Carve c;
     a.off_bar = c.take(8, 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_stage = c.take(a.slots * (a.dch + 4) * 4, 128);
+    a.off_stage = c.take(g4 ? a.slots / 4 * a.gpitch * 4 : a.slots * (a.dch + 4) * 4, 128);
+    a.off_rowid = c.take(g4 ? 32 * 4 : 0);
     a.warp_smem = round_up(c.total, 128);
     const int wpc = std::max(1, std::min(kGrWarps, env_int("TSDG_GR_WARPS", 1)));
     const size_t smem = (size_t)a.warp_smem * wpc;
     using GrKernel = void (*)(GrArgs);
     const bool tma = !env_is("TSDG_STAGE", "ldgsts");
     GrKernel kern;
-    if (idx->metric == 0)
+    if (g4)
+        kern = fast ? greedy_walk_kernel<0, true, kStageG4> : greedy_walk_kernel<0, false, kStageG4>;
+    else if (idx->metric == 0)
         kern = fast ? (tma ? greedy_walk_kernel<0, true, kStageTma> : greedy_walk_kernel<0, true, kStageLdgsts>)
                     : (tma ? greedy_walk_kernel<0, false, kStageTma> : greedy_walk_kernel<0, false, kStageLdgsts>);
     else if (idx->metric == 1)
