@@ -341,32 +341,33 @@ __device__ __forceinline__ void row_prefetch(const BfArgs& a, bool want, uint32_
     }
 }
 
-// Paired mode (two warps, one query): the leader warp runs the search; at every row
-// evaluation of more than B rows the helper warp takes the rows past the leader's
-// share.  ctl (shared memory): [0] command (1 evaluate, 0 exit), [1] rows, [2] the
-// leader's share (a multiple of B), [3] the current query.  One evaluation = one
-// "go" and one "done" barrier on both warps — the non-.aligned named barrier 1 (the
-// two warps reach it from different code), never __syncthreads().
-__device__ __forceinline__ void pair_barrier() {
-    asm volatile("barrier.sync 1, 64;" ::: "memory");
+// Group mode (GRP = 2 or 4 warps, one query): the leader warp runs the search; at
+// every row evaluation of more than B rows the helper warps take the rows past the
+// leader's share, share rows each.  ctl (shared memory): [0] command (1 evaluate,
+// 0 exit), [1] rows, [2] the share (a multiple of B), [3] the current query.  One
+// evaluation = one "go" and one "done" barrier on all GRP warps — the non-.aligned
+// named barrier 1 (the warps reach it from different code), never __syncthreads().
+template <int GRP>
+__device__ __forceinline__ void group_barrier() {
+    asm volatile("barrier.sync 1, %0;" ::"n"(GRP * 32) : "memory");
 }
-template <int METRIC, int B, int SEG, bool PIPE, bool PAIR>
+template <int METRIC, int B, int SEG, bool PIPE, int GRP>
 __device__ __forceinline__ void coop_eval(const FastGeom& g, const uint32_t* lst, float* dl,
                                           uint32_t cnt, ulonglong2 q, int lane,
                                           volatile uint32_t* ctl) {
-    if (!PAIR || cnt <= (uint32_t)B) {
+    if (GRP == 1 || cnt <= (uint32_t)B) {
         eval_list<METRIC, B, SEG, PIPE>(g, lst, dl, cnt, q, lane);
         return;
     }
-    const uint32_t h = ((cnt + 1) / 2 + B - 1) / B * B;  // < cnt when cnt > B
+    const uint32_t share = ((cnt + GRP - 1) / GRP + B - 1) / B * B;  // < cnt when cnt > B
     if (lane == 0) {
         ctl[0] = 1u;
         ctl[1] = cnt;
-        ctl[2] = h;
+        ctl[2] = share;
     }
-    pair_barrier();  // go
-    eval_list<METRIC, B, SEG, PIPE>(g, lst, dl, h, q, lane);
-    pair_barrier();  // done: the helper's dl entries are visible
+    group_barrier<GRP>();  // go
+    eval_list<METRIC, B, SEG, PIPE>(g, lst, dl, min(share, cnt), q, lane);
+    group_barrier<GRP>();  // done: the helpers' dl entries are visible
 }
 
 // Admission replay of one 32-edge chunk in edge order (bestfirst_search.cpp:85-96).
@@ -428,14 +429,15 @@ __device__ __forceinline__ void admit_chunk(const BfArgs& a, const FastCV& cv, c
 // MINB = resident CTAs per SM the register cap is set for: 12 -> 80 registers
 // (24 warps / SM), 16 -> 64 registers (32 warps / SM).
 //
-// PAIR: the CTA's two warps search ONE query together (leader + helper, coop_eval):
-// for batches smaller than the resident query slots (a rank's slice of a strong-scaled
-// batch), where one warp per query leaves most of the GPU idle.
-template <int METRIC, int B, int SEG, int MINB, bool PIPE, bool PAIR>
-__global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const BfArgs a) {
+// GRP > 1: the CTA's GRP warps search ONE query together (leader + helpers,
+// coop_eval): for batches smaller than the resident query slots (a rank's slice of a
+// strong-scaled batch), where one warp per query leaves most of the GPU idle.
+template <int METRIC, int B, int SEG, int MINB, bool PIPE, int GRP>
+__global__ void __launch_bounds__((GRP == 4 ? 4 : kFastWarps) * 32, GRP == 4 ? MINB / 2 : MINB)
+    bf_fast_kernel(const BfArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
-    unsigned char* ws = smem_raw + (PAIR ? 0u : (threadIdx.x >> 5) * a.warp_smem);
+    unsigned char* ws = smem_raw + (GRP > 1 ? 0u : (threadIdx.x >> 5) * a.warp_smem);
     volatile uint32_t* ctl = reinterpret_cast<volatile uint32_t*>(smem_raw + a.warp_smem);
     FastCV cv;
     cv.cid = reinterpret_cast<uint32_t*>(ws + a.off_cid);
@@ -453,21 +455,23 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
     const float kInf = __int_as_float(0x7f800000);
     const uint32_t seg_words = a.m * kSegPitch;  // multiple of 4
 
-    if (PAIR && (threadIdx.x >> 5) == 1) {  // helper warp
+    if (GRP > 1 && (threadIdx.x >> 5) != 0) {  // helper warp
+        const uint32_t hw = threadIdx.x >> 5;
         uint32_t cur = kInvalid;
         ulonglong2 q = make_ulonglong2(0ull, 0ull);
         for (;;) {
-            pair_barrier();  // go
+            group_barrier<GRP>();  // go
             if (ctl[0] == 0u) break;
-            const uint32_t qi = ctl[3], cnt = ctl[1], h = ctl[2];
+            const uint32_t qi = ctl[3], cnt = ctl[1], share = ctl[2];
             if (SEG != 0 && qi != cur) {
                 cur = qi;
                 const float* gq = a.queries + (size_t)qi * a.d;
                 q = (uint32_t)lane < g.ld4 ? *reinterpret_cast<const ulonglong2*>(gq + 4 * lane)
                                            : make_ulonglong2(0ull, 0ull);
             }
-            eval_list<METRIC, B, SEG, PIPE>(g, lst + h, dl + h, cnt - h, q, lane);
-            pair_barrier();  // done
+            const uint32_t b0 = hw * share;
+            if (b0 < cnt) eval_list<METRIC, B, SEG, PIPE>(g, lst + b0, dl + b0, min(cnt - b0, share), q, lane);
+            group_barrier<GRP>();  // done
         }
         return;
     }
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
         if (lane == 0) qi = atomicAdd(a.work_counter, 1u) - a.work_base;
         qi = __shfl_sync(kFull, qi, 0);
         if (qi >= a.nq) break;
-        if (PAIR && lane == 0) ctl[3] = qi;
+        if (GRP > 1 && lane == 0) ctl[3] = qi;
 
         const float* gq = a.queries + (size_t)qi * a.d;
         ulonglong2 q = make_ulonglong2(0ull, 0ull);
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
         lst[lane] = v0;
         if (a.prefetch & 1u) row_prefetch(a, lane >= B, v0, g.rowbytes);
         __syncwarp();
-        coop_eval<METRIC, B, SEG, PIPE, PAIR>(g, lst, dl, 32, q, lane, ctl);
+        coop_eval<METRIC, B, SEG, PIPE, GRP>(g, lst, dl, 32, q, lane, ctl);
         __syncwarp();
         float sd = dl[lane];
         uint32_t si = v0;
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
                     row_prefetch(a, need0 && rk0 >= (uint32_t)B, e0, g.rowbytes);
                     row_prefetch(a, need1 && rk1 >= (uint32_t)B, e1, g.rowbytes);
                 }
-                coop_eval<METRIC, B, SEG, PIPE, PAIR>(g, lst, dl, cnt, q, lane, ctl);
+                coop_eval<METRIC, B, SEG, PIPE, GRP>(g, lst, dl, cnt, q, lane, ctl);
                 __syncwarp();
                 float dist0 = need0 ? dl[rk0] : kInf;
                 float dist1 = need1 ? dl[rk1] : kInf;
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
                         uint32_t r0, r1;
                         __syncwarp();
                         const uint32_t rc = compact2(lst, rv, e1, false, 0u, r0, r1, lane, B);
-                        coop_eval<METRIC, B, SEG, PIPE, PAIR>(g, lst, dl, rc, q, lane, ctl);
+                        coop_eval<METRIC, B, SEG, PIPE, GRP>(g, lst, dl, rc, q, lane, ctl);
                         __syncwarp();
                         if (rv) dist1 = dl[r0];
                         evals += rc;
@@ -611,9 +615,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, MINB) bf_fast_kernel(const Bf
         }
         __syncwarp();
     }
-    if (PAIR) {  // release the helper
+    if (GRP > 1) {  // release the helpers
         if (lane == 0) ctl[0] = 0u;
-        pair_barrier();
+        group_barrier<GRP>();
     }
 }
 
@@ -627,7 +631,8 @@ using BfFastKernel = void (*)(BfArgs);
 //           5: B = 8 two-stage, 96 registers
 //           6: B = 4, 64 registers
 //           7: B = 4, 80 registers
-// pair: the two-warps-per-query form (default variant only).
-BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant, bool pair = false);
+// grp: warps per query (1; 2 / 4 = the group forms, default variant only; a group
+// launch has 32 * grp threads per CTA, one query per CTA).
+BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant, int grp = 1);
 
 }  // namespace tsdg_dev

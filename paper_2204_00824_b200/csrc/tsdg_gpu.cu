@@ -467,24 +467,29 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         const bool reg_q = idx->ld <= 128 && idx->ld == idx->d &&
                            (reinterpret_cast<uintptr_t>(d_queries) & 15u) == 0;
         const int seg = reg_q ? (idx->ld == 128 ? 1 : 2) : 0;
-        // Paired form (two warps per query) when the batch leaves most resident query
-        // slots empty: fewer queries than one CTA per slot of the one-warp-per-query
-        // launch (a strong-scaled rank's slice).  TSDG_FAST_PAIR=0 / 1 forces.
+        // Group forms (2 or 4 warps per query) when the batch leaves most resident
+        // query slots empty (a strong-scaled rank's slice): pairs below one query per
+        // CTA slot of the one-warp-per-query launch.  TSDG_FAST_GROUP=1|2|4 (or
+        // TSDG_FAST_PAIR=0|1) forces.
         const BfKernel single = bf_fast_kernel_for(idx->metric, seg, env_int("TSDG_FAST_VARIANT", 0));
         const size_t smem1 = (size_t)a.warp_smem * kFastWarps;
         set_smem(reinterpret_cast<const void*>(single), smem1, "cudaFuncSetAttribute(bf_fast)");
         const int slots = grid_for(single, kFastWarps * 32, smem1, idx->sm_count, 0xFFFFFFFFu, 1);
+        int grp = nq <= (uint32_t)slots ? 2 : 1;
         const int pair_env = env_int("TSDG_FAST_PAIR", -1);
-        const bool pair = pair_env >= 0 ? pair_env == 1 : nq <= (uint32_t)slots;
-        const BfKernel kern = pair ? bf_fast_kernel_for(idx->metric, seg, 0, true) : single;
-        const size_t smem = pair ? (size_t)a.warp_smem + 16 : smem1;
-        if (pair) set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast pair)");
+        if (pair_env >= 0) grp = pair_env == 1 ? 2 : 1;
+        const int grp_env = env_int("TSDG_FAST_GROUP", 0);
+        if (grp_env == 1 || grp_env == 2 || grp_env == 4) grp = grp_env;
+        const BfKernel kern = grp > 1 ? bf_fast_kernel_for(idx->metric, seg, 0, grp) : single;
+        const size_t smem = grp > 1 ? (size_t)a.warp_smem + 16 : smem1;
+        const int threads = (grp == 4 ? 4 : kFastWarps) * 32;
+        if (grp > 1) set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(bf_fast group)");
         // work fetches: one per query plus one final per fetching warp (the leader only
-        // in the paired form)
-        const int grid = pair ? grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, 1)
-                              : grid_for(kern, kFastWarps * 32, smem, idx->sm_count, nq, kFastWarps);
-        kern<<<grid, kFastWarps * 32, smem, st>>>(a);
-        commit_counter(idx, tk, nq, (uint64_t)grid * (pair ? 1 : kFastWarps), st);
+        // in the group forms)
+        const int grid = grp > 1 ? grid_for(kern, threads, smem, idx->sm_count, nq, 1)
+                                 : grid_for(kern, threads, smem, idx->sm_count, nq, kFastWarps);
+        kern<<<grid, threads, smem, st>>>(a);
+        commit_counter(idx, tk, nq, (uint64_t)grid * (grp > 1 ? 1 : kFastWarps), st);
         g_launches++;
         cuda_check(cudaGetLastError(), "bf_fast_kernel launch");
         return;
@@ -574,8 +579,10 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
     // row staging: gather4 tensor copies for L2 rows of <= dch floats (C2, t0=10,
     // batch 256 / 1024 / 4096: 162 / 388 / 1304 vs 180 / 430 / 1437 us with one bulk
     // copy per row, bit-exact); TSDG_GR_STAGE=tma forces per-row copies
-    const bool g4 = !env_is("TSDG_GR_STAGE", "tma") && idx->ld <= a.dch && idx->metric == 0 &&
-                    !env_is("TSDG_STAGE", "ldgsts") && (a.tmap = vectors_tmap(idx, a.dch + 4, st)) != nullptr;
+    if (!env_is("TSDG_GR_STAGE", "tma") && !env_is("TSDG_STAGE", "ldgsts") && idx->ld <= a.dch &&
+        idx->metric == 0)
+        a.tmap = vectors_tmap(idx, a.dch + 4, st);
+    const bool g4 = a.tmap != nullptr;
     a.gpitch = round_up(4 * (a.dch + 4), 32);
     Carve c;
     a.off_bar = c.take(8, 8);

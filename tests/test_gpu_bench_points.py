@@ -202,17 +202,19 @@ def test_sharded_standin_device_merge_equals_oracle(orc):
 
 
 def test_c2_fast_paired_kernel_equals_single(c2, monkeypatch):
-    """Two warps per query (the form routed for small slices: fewer queries than
-    resident CTA slots) computes every row exactly as one warp does, so its results
-    equal the one-warp-per-query fast kernel's bit for bit, for any batch size."""
+    """Two or four warps per query (the group forms routed for small slices: fewer
+    queries than resident CTA slots) compute every row exactly as one warp does, so
+    their results equal the one-warp-per-query fast kernel's bit for bit, for any
+    batch size."""
     ds, idx, g = c2
     p = BestFirstParams(**C2_PARAMS)
     for lo, hi in ((0, 1250), (1250, 1260), (3000, 8000)):
         q = ds.queries[lo:hi]
         got = {}
-        for pair in ("0", "1"):
-            monkeypatch.setenv("TSDG_FAST_PAIR", pair)
-            got[pair] = idx.search_bestfirst(q, p, query_index_base=lo, mode=_native.MODE_FAST)
-        np.testing.assert_array_equal(got["1"].ids, got["0"].ids)
-        np.testing.assert_array_equal(got["1"].dists.view(np.uint32), got["0"].dists.view(np.uint32))
-        np.testing.assert_array_equal(got["1"].stats, got["0"].stats)
+        for grp in ("1", "2", "4"):
+            monkeypatch.setenv("TSDG_FAST_GROUP", grp)
+            got[grp] = idx.search_bestfirst(q, p, query_index_base=lo, mode=_native.MODE_FAST)
+        for grp in ("2", "4"):
+            np.testing.assert_array_equal(got[grp].ids, got["1"].ids)
+            np.testing.assert_array_equal(got[grp].dists.view(np.uint32), got["1"].dists.view(np.uint32))
+            np.testing.assert_array_equal(got[grp].stats, got["1"].stats)

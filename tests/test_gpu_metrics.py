@@ -280,19 +280,21 @@ def test_many_overlapping_device_launches_on_two_streams(fixtures, index):
 
 @pytest.mark.parametrize("name", ["syn2k", "lowlid3k"])
 def test_fast_paired_kernel_equals_single_on_fixtures(fixtures, index, monkeypatch, name):
-    """The paired fast kernel (two warps per query) on the golden fixtures (d = 32, the
-    query-in-registers class below 128 floats) equals the single-warp fast kernel."""
+    """The group fast kernels (two / four warps per query) on the golden fixtures
+    (d = 32, the query-in-registers class below 128 floats) equal the single-warp fast
+    kernel."""
     from paper_2204_00824_b200.search import BestFirstParams
     g, b, q = fixtures(name)
     idx = index(name)
     for pd in (dict(k=10, seed=7), dict(k=24, seed=3, m_segments=4, lambda_cut=10)):
         p = BestFirstParams(**pd)
         res = {}
-        for pair in ("0", "1"):
-            monkeypatch.setenv("TSDG_FAST_PAIR", pair)
-            res[pair] = idx.search_bestfirst(q, p, mode=_native.MODE_FAST)
-        np.testing.assert_array_equal(res["1"].ids, res["0"].ids)
-        np.testing.assert_array_equal(res["1"].dists.view(np.uint32), res["0"].dists.view(np.uint32))
+        for grp in ("1", "2", "4"):
+            monkeypatch.setenv("TSDG_FAST_GROUP", grp)
+            res[grp] = idx.search_bestfirst(q, p, mode=_native.MODE_FAST)
+        for grp in ("2", "4"):
+            np.testing.assert_array_equal(res[grp].ids, res["1"].ids)
+            np.testing.assert_array_equal(res[grp].dists.view(np.uint32), res["1"].dists.view(np.uint32))
 
 
 @pytest.mark.parametrize("env", [{"TSDG_FAST_VARIANT": str(v)} for v in range(8)]

@@ -31,8 +31,9 @@ for ws in (1, 2, 4, 8):
     ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     dd = torch.empty((nq, k), dtype=torch.float32, device="cuda")
     cc = torch.empty(nq, dtype=torch.int32, device="cuda")
-    for mode, pair in ((_native.MODE_FAST, "0"), (_native.MODE_FAST, "1"), (_native.MODE_DETERMINISTIC, "0")):
-        os.environ["TSDG_FAST_PAIR"] = pair
+    for mode, grp in ((_native.MODE_FAST, "1"), (_native.MODE_FAST, "2"), (_native.MODE_FAST, "4"),
+                      (_native.MODE_DETERMINISTIC, "1")):
+        os.environ["TSDG_FAST_GROUP"] = grp
 
         def step():
             idx.search_bestfirst_device(dq.data_ptr(), nq, p, ids.data_ptr(), dd.data_ptr(), cc.data_ptr(),
@@ -50,6 +51,6 @@ for ws in (1, 2, 4, 8):
             ts.append(a.elapsed_time(b))
         ms = float(np.median(ts))
         print(json.dumps({"gpus": ws, "queries_per_gpu": nq, "mode": "fast" if mode else "det",
-                          "paired": pair == "1" and mode == _native.MODE_FAST,
+                          "warps_per_query": int(grp) if mode == _native.MODE_FAST else 1,
                           "ms": ms, "qps_per_gpu": nq / ms * 1e3,
                           "projected_total_qps": ws * nq / ms * 1e3}), flush=True)
