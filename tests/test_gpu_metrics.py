@@ -336,3 +336,37 @@ def _c1():
         ds = datasets.load("c1_lowlid_100k")
         _C1.append((ds, search.GpuIndex.from_file(ds.graph_path, ds.base)))
     return _C1[0]
+
+
+@pytest.mark.parametrize("stage", ["tma", "g4", "ldgsts"])
+def test_row_staging_paths_bit_exact(tmp_path, monkeypatch, stage):
+    """Every row-staging path — one TMA bulk copy per row, TMA tile::gather4 tensor
+    copies (4 rows per instruction, partial last groups, box = padded row), cp.async —
+    in the deterministic best-first kernel and both greedy kernels reproduces the
+    oracle, on a 12-float row (box of 20 floats) under L2 and on the inner-product
+    fixture."""
+    from paper_2204_00824_b200 import search
+    for var in ("TSDG_STAGE", "TSDG_GC_STAGE"):
+        monkeypatch.setenv(var, stage)
+    monkeypatch.setenv("TSDG_GR_STAGE", "tma" if stage == "tma" else "g4")
+    orc = O.Oracle()
+    base, queries = datasets.make_synthetic_split(1200, 40, 12, 4, 0.3, 17)
+    knn = search.brute_force_knn(base, 16)
+    path = str(tmp_path / "d12.tsdg")
+    search.build(base, knn, 1.2, 9, 0, save_path=path)
+    cases = [(path, base, queries)]
+    with open(os.path.join(GOLDEN, "scan.json")) as f:
+        spec = json.load(f)["specs"]["b"]
+    b2, q2 = datasets.generate(spec)
+    cases.append((os.path.join(GOLDEN, "build_ip_b.tsdg"), b2, q2))
+    for p_, b, q in cases:
+        g = O.parse_tsdg(p_)
+        idx = search.GpuIndex.from_file(p_, b)
+        p = search.BestFirstParams(k=10, seed=3)
+        _same(idx.search_bestfirst(q, p), orc.large_batch(g, b, q, p))
+        for kern in ("cta", "warp"):
+            monkeypatch.setenv("TSDG_GREEDY", kern)
+            gp = search.GreedyParams(t0=5, seed=9)
+            _same(idx.search_greedy(q, 10, gp), orc.small_batch(g, b, q, 10, gp))
+        monkeypatch.delenv("TSDG_GREEDY")
+        idx.close()
