@@ -31,6 +31,8 @@
 //   goes to global memory; splits are merged per query by merge_splits_kernel.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "stage.cuh"  // f32x2 helpers, cp_async16
 
 namespace tsdg_dev {
@@ -47,10 +49,11 @@ constexpr uint32_t kScanQBuf = kScanDC * kScanQT;        // floats per query buf
 
 constexpr uint32_t kScanSortN = 128;  // per-warp sort scratch (entries)
 
-// Dynamic shared memory of exact_scan_kernel for candidate buffers of P entries.
+// Dynamic shared memory of exact_scan_kernel for candidate buffers of P entries (+
+// 1 KB to align the row buffers for the 128-byte TMA swizzle, + two mbarriers).
 constexpr size_t scan_smem_bytes(uint32_t P) {
-    return 2 * (size_t)(kScanRowBuf + kScanQBuf) * 4 + (size_t)kScanQT * P * 8 +
-           (size_t)(kScanThreads / 32) * kScanSortN * 8 + kScanQT * 16;
+    return 1024 + 2 * (size_t)(kScanRowBuf + kScanQBuf) * 4 + (size_t)kScanQT * P * 8 +
+           (size_t)(kScanThreads / 32) * kScanSortN * 8 + kScanQT * 16 + 8 + 16;
 }
 
 struct ScanArgs {
@@ -183,9 +186,19 @@ __device__ __forceinline__ void scan_prod(unsigned long long& tt, unsigned long 
     else tt = f2_fma(qq, f2_dup(b), nz);
 }
 
-template <int METRIC>
-__global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kernel(const ScanArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// TMA: the row chunks arrive by one 2-D tensor copy per chunk (box {32 dims, 128
+// rows}, 128-byte swizzle: 16-byte unit u of row r lands at unit u ^ (r & 7), so the
+// eight rows an LDS.128 phase reads sit in eight different bank groups), completion
+// counted on one mbarrier per buffer — instead of 8 cp.async (and their address
+// arithmetic) per thread per chunk.  Otherwise rows go by cp.async into 36-float
+// rows.
+template <int METRIC, bool TMA>
+__global__ void __launch_bounds__(kScanThreads, kScanMinBlocks)
+    exact_scan_kernel(const ScanArgs a, const __grid_constant__ CUtensorMap tm) {
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    // 1024-byte aligned start (offset from the shared array itself, so that the
+    // compiler keeps every access below in the shared state space)
+    unsigned char* smem = smem_dyn + ((1024u - (smem_addr(smem_dyn) & 1023u)) & 1023u);
     float* rs = reinterpret_cast<float*>(smem);                                      // [2][BT][RPitch]
     float* qs = rs + 2 * kScanRowBuf;                                                // [2][DC][QT]
     float* cd = qs + 2 * kScanQBuf;                                                  // [QT][P]
@@ -196,6 +209,7 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
     uint32_t* srt = cnt + kScanQT;                                                   // [QT] sorted prefix
     float* thr_d = reinterpret_cast<float*>(srt + kScanQT);                          // [QT]
     uint32_t* thr_i = reinterpret_cast<uint32_t*>(thr_d + kScanQT);                 // [QT]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(thr_i + kScanQT + ((smem_addr(thr_i + kScanQT) & 7u) ? 1 : 0));  // [2]
 
     const float kInf = __int_as_float(0x7f800000);
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -208,6 +222,13 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
         srt[tid] = 0;
         thr_d[tid] = kInf;
         thr_i[tid] = kInvalid;
+    }
+    if (TMA) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+        }
+        __syncthreads();
     }
     const unsigned long long nz = a.keep & 0x8000000080000000ull;  // (-0, -0), opaque
     const uint32_t nchunks = (a.d + kScanDC - 1) / kScanDC;
@@ -222,14 +243,25 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
     auto issue = [&](uint32_t s) {
         const uint32_t row0 = r_begin + (s / nchunks) * kScanBT, c0 = (s % nchunks) * kScanDC;
         float* rb = rs + (s & 1u) * kScanRowBuf;
+        if (TMA) {
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&bars[s & 1u], kScanBT * kScanDC * 4);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(rb)),
+                    "l"(&tm), "r"(c0), "r"(row0), "r"(smem_addr(&bars[s & 1u]))
+                    : "memory");
+            }
+        } else {
 #pragma unroll
-        for (uint32_t t = 0; t < (uint32_t)kScanRPT; ++t) {
-            const uint32_t f = tid + t * kScanThreads;
-            const uint32_t r = f >> 3, dim = c0 + (f & 7u) * 4;
-            if (row0 + r < r_end && dim < a.ld_b)
-                cp_async16(rb + r * kScanRPitch + (f & 7u) * 4, a.base + (size_t)(row0 + r) * a.ld_b + dim);
+            for (uint32_t t = 0; t < (uint32_t)kScanRPT; ++t) {
+                const uint32_t f = tid + t * kScanThreads;
+                const uint32_t r = f >> 3, dim = c0 + (f & 7u) * 4;
+                if (row0 + r < r_end && dim < a.ld_b)
+                    cp_async16(rb + r * kScanRPitch + (f & 7u) * 4, a.base + (size_t)(row0 + r) * a.ld_b + dim);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
         for (uint32_t t = 0; t < 2; ++t) {
             const uint32_t f = tid + t * kScanThreads;
@@ -265,10 +297,14 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
 #pragma unroll
             for (int i = 0; i < 2 * kScanRPT; ++i) acc[i] = 0ull;
         }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (TMA) mbar_wait(&bars[s & 1u], (s >> 1) & 1u);
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();  // step s staged by all; step s - 1 consumed by all
         if (s + 1 < steps) issue(s + 1);
-        const float* rb = rs + (s & 1u) * kScanRowBuf + tb * kScanRPitch;
+        // row tb + 16 i: TMA rows are kScanDC floats with the 16-byte units swizzled by
+        // (row & 7) = (tb & 7); cp.async rows are kScanRPitch floats, unswizzled
+        const uint32_t rp = TMA ? kScanDC : kScanRPitch, sw = TMA ? (tb & 7u) : 0u;
+        const float* rb = rs + (s & 1u) * kScanRowBuf + tb * rp;
         const float* qb = qs + (s & 1u) * kScanQBuf + 4 * tq;
         const uint32_t dims = min(kScanDC, a.d - c * kScanDC);
         if (dims == kScanDC) {
@@ -277,7 +313,7 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
                 float4 bv[kScanRPT];
 #pragma unroll
                 for (int i = 0; i < kScanRPT; ++i)
-                    bv[i] = *reinterpret_cast<const float4*>(rb + i * 16 * kScanRPitch + j4);
+                    bv[i] = *reinterpret_cast<const float4*>(rb + i * 16 * rp + (((j4 >> 2) ^ sw) << 2));
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + (j4 + jj) * kScanQT);
@@ -304,7 +340,7 @@ __global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) exact_scan_kerne
                 const ulonglong2 qv = *reinterpret_cast<const ulonglong2*>(qb + j * kScanQT);
 #pragma unroll
                 for (int i = 0; i < kScanRPT; ++i) {
-                    const float b = rb[i * 16 * kScanRPitch + j];
+                    const float b = rb[i * 16 * rp + ((((j >> 2) ^ sw) << 2) | (j & 3u))];
                     scan_step<METRIC>(acc[2 * i + 0], qv.x, b, nz);
                     scan_step<METRIC>(acc[2 * i + 1], qv.y, b, nz);
                 }

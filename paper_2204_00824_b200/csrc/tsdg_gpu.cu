@@ -617,9 +617,10 @@ void launch_walks(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, uint
 // ld are out of bounds and arrive as zeros).  Encoded once per index through the
 // driver entry point (no libcuda link); nullptr when the driver rejects it (the
 // kernels then stage with one bulk copy per row).  Caller holds idx->mu.
-const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
-    if (idx->tmap_tried) return idx->tmap_box == box ? idx->tmap : nullptr;
-    idx->tmap_tried = true;
+// 2-D fp32 tensor map {cols, rows} with row stride ld floats and box {bc, br};
+// false when the driver entry point or the encoding is unavailable.
+bool encode_tmap_2d(CUtensorMap* tm, const float* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                    uint32_t bc, uint32_t br, CUtensorMapSwizzle swz) {
     using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -633,15 +634,23 @@ const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
         (void)cudaGetLastError();
         return reinterpret_cast<Encode>(fn);
     }();
-    if (!enc || box > 256 || (box * 4) % 16 || idx->n == 0) return nullptr;
-    alignas(64) CUtensorMap tm;
-    const cuuint64_t gdim[2] = {idx->ld, idx->n};
-    const cuuint64_t gstride[1] = {(cuuint64_t)idx->ld * 4};
-    const cuuint32_t bdim[2] = {box, 1};
+    if (!enc || rows == 0 || bc > 256 || br > 256 || (bc * 4) % 16 || (ld * 4) % 16 ||
+        (reinterpret_cast<uintptr_t>(base) & 15u))
+        return false;
+    const cuuint64_t gdim[2] = {cols, rows};
+    const cuuint64_t gstride[1] = {ld * 4};
+    const cuuint32_t bdim[2] = {bc, br};
     const cuuint32_t estride[2] = {1, 1};
-    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, idx->vec, gdim, gstride, bdim, estride,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, bdim, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
+    if (idx->tmap_tried) return idx->tmap_box == box ? idx->tmap : nullptr;
+    idx->tmap_tried = true;
+    alignas(64) CUtensorMap tm;
+    if (!encode_tmap_2d(&tm, idx->vec, idx->ld, idx->n, idx->ld, box, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
         return nullptr;
     void* dev = nullptr;
     cuda_check(cudaMalloc(&dev, sizeof(CUtensorMap)), "cudaMalloc(tensor map)");
@@ -886,8 +895,19 @@ void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const flo
     a.self_base = self_base;
     a.keep = ~0ull;
     const size_t smem = scan_smem_bytes(a.P);
-    void (*kern)(ScanArgs) = metric == 0 ? exact_scan_kernel<0>
-                             : metric == 1 ? exact_scan_kernel<1> : exact_scan_kernel<2>;
+    // row chunks by one TMA tensor copy each (128-byte swizzle) when the base can be
+    // described by a tensor map (16-byte aligned, fewer than 2^31 rows: TMA
+    // coordinates are signed 32-bit); else 8 cp.async per thread.  TSDG_SCAN_TMA=0
+    // forces cp.async.
+    alignas(64) CUtensorMap tm{};
+    const bool tma = !env_is("TSDG_SCAN_TMA", "0") && n < (1u << 31) &&
+                     encode_tmap_2d(&tm, d_base, ld_b, n, ld_b, kScanDC, kScanBT, CU_TENSOR_MAP_SWIZZLE_128B);
+    using ScanKernel = void (*)(ScanArgs, CUtensorMap);
+    ScanKernel kern;
+    if (tma) kern = metric == 0 ? exact_scan_kernel<0, true> : metric == 1 ? exact_scan_kernel<1, true>
+                                                                           : exact_scan_kernel<2, true>;
+    else kern = metric == 0 ? exact_scan_kernel<0, false> : metric == 1 ? exact_scan_kernel<1, false>
+                                                                        : exact_scan_kernel<2, false>;
     set_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(exact_scan)");
     const int per_sm = occupancy(reinterpret_cast<const void*>(kern), kScanThreads, smem);
     const uint32_t slots = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
@@ -909,7 +929,7 @@ void launch_exact_topk(const float* d_base, uint32_t n, uint32_t ld_b, const flo
     }
     a.out_ids = tids;
     a.out_dists = tdist;
-    kern<<<dim3(qtiles, S), kScanThreads, smem, st>>>(a);
+    kern<<<dim3(qtiles, S), kScanThreads, smem, st>>>(a, tm);
     g_launches++;
     cuda_check(cudaGetLastError(), "exact_scan_kernel launch");
     if (S > 1) {
