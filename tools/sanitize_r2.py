@@ -1,6 +1,7 @@
 """Small workloads over the round-2 kernels for compute-sanitizer (memcheck /
-racecheck / synccheck): GPU nn_descent, the fast best-first kernel in its single and
-paired forms, the greedy cluster kernel with the merge warp, the sharded index.
+racecheck / synccheck): GPU nn_descent, the exact scan, the fast best-first kernel in
+its single and paired forms, the greedy cluster kernel with the merge warp (gather4
+staging by default), the sharded index.
 
     compute-sanitizer --tool memcheck python tools/sanitize_r2.py"""
 import os
@@ -17,6 +18,8 @@ from paper_2204_00824_b200.search import BestFirstParams, GreedyParams  # noqa: 
 base, queries = datasets.make_synthetic_split(2000, 200, 32, 8, 0.2, 11)
 g = search.nn_descent(base[:1500], 16, 2, 0.5, 7)
 print("nn_descent", g.ids.shape, flush=True)
+gt = search.ground_truth(base, queries[:40], 10)  # exact scan, TMA row tiles
+print("exact scan", gt.ids.shape, flush=True)
 idx = search.GpuIndex.from_file(os.path.join(ROOT, "tests", "golden", "syn2k.tsdg"), base)
 p = BestFirstParams(k=10, seed=7)
 for pair in ("0", "1"):
