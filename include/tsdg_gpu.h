@@ -28,8 +28,9 @@
  *   TSDG_E2E_CHUNKS, TSDG_E2E_FIRST   copy-pipeline chunking (2 chunks, first 25%)
  *   TSDG_FAST_KERNEL=staged|register  fast best-first kernel choice (default: the
  *                           register-direct kernel for rows <= 128 floats, k <= 31)
- *   TSDG_FAST_PAIR=0|1      force the single / paired (two warps per query) fast
- *                           kernel (default: paired below one query per CTA slot)
+ *   TSDG_FAST_PAIR=0|1, TSDG_FAST_GROUP=1|2|4   force the single / group (two or
+ *                           four warps per query) fast kernel (default: pairs below
+ *                           one query per CTA slot)
  *   TSDG_FAST_VARIANT, TSDG_FAST_PREFETCH   fast-kernel tuning variants (bf_fast.cu)
  *   TSDG_STAGE=g4|tma|ldgsts, TSDG_SLOTS, TSDG_BF_WARPS, TSDG_PREFETCH, TSDG_BATCH_MIN
  *                           staged best-first kernel: staging path (default: TMA
@@ -37,8 +38,8 @@
  *                           <= 128 floats, else one bulk copy per row) / slots / warps
  *   TSDG_GREEDY=cta|warp, TSDG_GREEDY_CTA_MAX_WALKS   greedy kernel routing
  *   TSDG_GC_STAGE=g4|tma|ldgsts, TSDG_GC_MERGE_WARP, TSDG_GC_SLICE, TSDG_GC_ADJ_PREFETCH,
- *   TSDG_GR_WARPS           greedy kernels' staging / warp roles
- *   TSDG_SCAN_SPLITS        exact-scan base splits
+ *   TSDG_GR_WARPS, TSDG_GR_STAGE=g4|tma   greedy kernels' staging / warp roles
+ *   TSDG_SCAN_SPLITS, TSDG_SCAN_TMA=0   exact-scan base splits / cp.async row tiles
  *   TSDG_DEBUG_PATH=1, TSDG_LOAD_TRACE=1   diagnostics on stderr
  */
 #ifndef TSDG_GPU_H
