@@ -18,6 +18,7 @@ static BfFastKernel pick(int variant, int grp) {
             case 5: return bf_fast_kernel<METRIC, 8, SEG, 10, true, 1>;
             case 6: return bf_fast_kernel<METRIC, 4, SEG, 16, false, 1>;
             case 7: return bf_fast_kernel<METRIC, 4, SEG, 12, false, 1>;
+            case 8: return bf_fast_kernel<METRIC, 8, SEG, 14, false, 1>;
             default: break;
         }
     }

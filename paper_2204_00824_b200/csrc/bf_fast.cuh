@@ -623,14 +623,15 @@ __global__ void __launch_bounds__((GRP == 4 ? 4 : kFastWarps) * 32, GRP == 4 ? M
 
 using BfFastKernel = void (*)(BfArgs);
 // bf_fast.cu: the instantiation for (metric, row class, variant)
-//   variant 0: B = 8, 80 registers (24 warps / SM)      [default]
-//           1: B = 8, 64 registers (32 warps / SM)
+//   variant 0: B = 8, 80 registers (24 warps / SM)      [default, other row classes]
+//           1: B = 8, 64 registers (32 warps / SM)      [default, L2 / 128-float rows]
 //           2: B = 16, 80 registers
 //           3: B = 16, 96 registers (20 warps / SM)
 //           4: B = 8 two-stage, 80 registers
 //           5: B = 8 two-stage, 96 registers
 //           6: B = 4, 64 registers
 //           7: B = 4, 80 registers
+//           8: B = 8, 72 registers (28 warps / SM)
 // grp: warps per query (1; 2 / 4 = the group forms, default variant only; a group
 // launch has 32 * grp threads per CTA, one query per CTA).
 BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant, int grp = 1);

@@ -471,7 +471,11 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         // query slots empty (a strong-scaled rank's slice): pairs below one query per
         // CTA slot of the one-warp-per-query launch.  TSDG_FAST_GROUP=1|2|4 (or
         // TSDG_FAST_PAIR=0|1) forces.
-        const BfKernel single = bf_fast_kernel_for(idx->metric, seg, env_int("TSDG_FAST_VARIANT", 0));
+        // variant 1 (64 registers, 32 warps / SM) for L2 over 128-float rows: C2 0.7025
+        // vs 0.7086 ms for variant 0 (80 registers; before the REDUX arg-min variant 1
+        // spilled and was slower, 0.863 ms) — profiles/fast_variants_r2b.jsonl
+        const int variant = env_int("TSDG_FAST_VARIANT", idx->metric == 0 && seg == 1 ? 1 : 0);
+        const BfKernel single = bf_fast_kernel_for(idx->metric, seg, variant);
         const size_t smem1 = (size_t)a.warp_smem * kFastWarps;
         set_smem(reinterpret_cast<const void*>(single), smem1, "cudaFuncSetAttribute(bf_fast)");
         const int slots = grid_for(single, kFastWarps * 32, smem1, idx->sm_count, 0xFFFFFFFFu, 1);

@@ -297,7 +297,7 @@ def test_fast_paired_kernel_equals_single_on_fixtures(fixtures, index, monkeypat
             np.testing.assert_array_equal(res[grp].dists.view(np.uint32), res["1"].dists.view(np.uint32))
 
 
-@pytest.mark.parametrize("env", [{"TSDG_FAST_VARIANT": str(v)} for v in range(8)]
+@pytest.mark.parametrize("env", [{"TSDG_FAST_VARIANT": str(v)} for v in range(9)]
                          + [{"TSDG_FAST_PREFETCH": p} for p in ("0", "2", "5")]
                          + [{"TSDG_FAST_KERNEL": "staged"}, {"TSDG_FAST_KERNEL": "register"}])
 def test_fast_kernel_knobs_keep_recall(fixtures, index, golden, monkeypatch, env):
