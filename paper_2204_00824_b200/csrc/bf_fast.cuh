@@ -632,8 +632,8 @@ using BfFastKernel = void (*)(BfArgs);
 //           6: B = 4, 64 registers
 //           7: B = 4, 80 registers
 //           8: B = 8, 72 registers (28 warps / SM)
-// grp: warps per query (1; 2 / 4 = the group forms, default variant only; a group
-// launch has 32 * grp threads per CTA, one query per CTA).
+// grp: warps per query (1; 2 / 4 = the group forms, in variant 0's register budget;
+// a group launch has 32 * grp threads per CTA, one query per CTA).
 BfFastKernel bf_fast_kernel_for(int metric, int seg, int variant, int grp = 1);
 
 }  // namespace tsdg_dev

@@ -484,6 +484,8 @@ void launch_bestfirst(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq, 
         if (pair_env >= 0) grp = pair_env == 1 ? 2 : 1;
         const int grp_env = env_int("TSDG_FAST_GROUP", 0);
         if (grp_env == 1 || grp_env == 2 || grp_env == 4) grp = grp_env;
+        // (the group forms keep the 80-register budget: a pair in 64 registers took
+        // 0.249 vs 0.208 ms for a 1250-query slice)
         const BfKernel kern = grp > 1 ? bf_fast_kernel_for(idx->metric, seg, 0, grp) : single;
         const size_t smem = grp > 1 ? (size_t)a.warp_smem + 16 : smem1;
         const int threads = (grp == 4 ? 4 : kFastWarps) * 32;
