@@ -74,8 +74,12 @@ __device__ __forceinline__ bool warp_merge_halves(float& rd, uint32_t& ri, float
     // repeated ids: against R_ij, and within the newcomers (adjacent once sorted)
     const uint32_t prev = __shfl_up_sync(kFull, ti, 1);
     bool dup = lane > 0 && prev == ti;
-#pragma unroll 8
-    for (int t = 0; t < 32; ++t) dup |= __shfl_sync(kFull, ri, t) == ti;
+    // membership of the 16 candidates (lanes 0-15) in R_ij: two MATCH.ANY rounds, the
+    // upper 16 lanes carrying R_ij's lower / upper half (instead of 32 broadcasts)
+    const uint32_t r_lo = __shfl_sync(kFull, ri, lane & 15), r_hi = __shfl_sync(kFull, ri, (lane & 15) + 16);
+    const unsigned m_lo = __match_any_sync(kFull, lane < 16 ? ti : r_lo);
+    const unsigned m_hi = __match_any_sync(kFull, lane < 16 ? ti : r_hi);
+    dup |= ((m_lo | m_hi) & 0xFFFF0000u) != 0u;
     const unsigned vm = __ballot_sync(kFull, lane < 16 && ti != kInvalid && !dup);
     // lane L takes newcomer number 31 - L (the reversed, compacted newcomer list)
     const uint32_t want = 31u - (uint32_t)lane;
