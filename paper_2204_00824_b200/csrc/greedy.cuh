@@ -210,13 +210,19 @@ __device__ __forceinline__ uint32_t warp_kway_unique(const float* ld, const uint
                                                      Out out) {
     const float kInf = __int_as_float(0x7f800000);
     uint32_t pos = 0;
-    float hd = kInf;
-    uint32_t hi = kInvalid;
     const bool mine = (uint32_t)lane < nlists;
-    if (mine && len > 0) {
-        hi = li[(size_t)lane * stride];
-        hd = hi != kInvalid ? ld[(size_t)lane * stride] : kInf;
-    }
+    // head (pos) and the entry after it, loaded one step ahead so that advancing a
+    // list is a register move (the distance of an invalid id is never used: the key
+    // below ignores it)
+    auto fetch = [&](uint32_t p, float& d, uint32_t& i) {
+        const bool ok = mine && p < len;
+        i = ok ? li[(size_t)lane * stride + p] : kInvalid;
+        d = ok ? ld[(size_t)lane * stride + p] : kInf;
+    };
+    float hd, nd;
+    uint32_t hi, ni;
+    fetch(0, hd, hi);
+    fetch(1, nd, ni);
     uint32_t cnt = 0;
     while (cnt < k) {
         // closer()-minimum of the heads by two REDUX.MIN: the distance (as an
@@ -235,8 +241,9 @@ __device__ __forceinline__ uint32_t warp_kway_unique(const float* ld, const uint
         ++cnt;
         if (hi == bi) {
             ++pos;
-            hi = pos < len ? li[(size_t)lane * stride + pos] : kInvalid;
-            hd = hi != kInvalid ? ld[(size_t)lane * stride + pos] : kInf;
+            hd = nd;
+            hi = ni;
+            fetch(pos + 1, nd, ni);
         }
     }
     return cnt;
