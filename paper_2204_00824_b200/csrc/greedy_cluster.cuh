@@ -55,6 +55,8 @@ struct GcArgs {
     uint32_t early_next;    // 1: next node from the evaluating warps' minima
     uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
                             // evaluated node (the next hop's u is one of them)
+    uint32_t spec_next;     // 1: the evaluating warps run hop t+1 while warp 0 merges
+                            // hop t (dropped if that merge changed nothing)
     uint32_t npow2;      // pool size for the in-cluster merge
     uint32_t dch, slots;
     uint32_t stage;       // host: StageKind the kernel was chosen for
@@ -66,14 +68,17 @@ struct GcArgs {
 struct GcCtl {
     uint32_t u;
     uint32_t improved;
+    uint32_t imp[2];  // spec_next: hop t's merge result in imp[t & 1]
     uint32_t hops;
     uint32_t evals;
     uint32_t u_next;  // next node, published before the merge (L2 warm-up)
     // per evaluating warp: its smallest distance of the hop (orderable key), the id
-    // holding it and how many candidates share it (the early next-node pick)
-    uint32_t best_k[4];
-    uint32_t best_i[4];
-    uint32_t best_n[4];
+    // holding it and how many candidates share it (the early next-node pick); two
+    // sets, by hop parity (with spec_next the next hop's values arrive while this
+    // hop's are still being read)
+    uint32_t best_k[8];
+    uint32_t best_i[8];
+    uint32_t best_n[8];
 };
 
 // float -> uint32 with the same order (closer() on distances; -0 == +0)
@@ -109,8 +114,8 @@ struct GcSmem {
     uint32_t* pool_i;
     uint32_t* scan;
     uint32_t* walk_cnt;  // rank 0: 2 x t0 (hops, evals) pushed by the walks
-    float* pos_d;        // this hop's distance / id by adjacency position (R entries)
-    uint32_t* pos_i;
+    float* pos_d;        // distance / id by adjacency position (R entries each), two
+    uint32_t* pos_i;     // sets by hop parity: set b at pos_d + 2 R b, pos_i + 2 R b
 };
 
 __device__ __forceinline__ GcSmem gc_smem(const GcArgs& a, unsigned char* smem_raw) {
@@ -173,6 +178,8 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         if (lane == 0) {
             ctl->u = si;
             ctl->improved = 1;
+            ctl->imp[0] = 1;
+            ctl->imp[1] = 1;
             ctl->hops = 0;
             ctl->evals = 32;
         }
@@ -201,9 +208,16 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     const uint32_t SL = a.slice, P = nev * SL;
     const bool lane_on = evaluates && (uint32_t)lane < SL;
     const uint32_t j0 = lane_on ? ew * SL + lane : 0xFFFFFFFFu;  // round-0 position
-    float* pos_d = m.pos_d;
-    uint32_t* pos_i = m.pos_i;
     uint32_t deg = 0, e0 = kInvalid;
+    // Speculative next hop (a.spec_next, with the merge warp, the early pick and the
+    // pipelined gathers): there is no barrier at the end of a hop; warps 1-3 start
+    // hop t+1 (its first slice is already in flight) while warp 0 still merges hop
+    // t, and hop t+1's first barrier tells everyone whether that merge improved R_ij
+    // — if not, the walk ended after hop t and hop t+1 is dropped (not counted, not
+    // merged), so results and counters are the sequential loop's.  pos_* and the
+    // early-pick words are double-buffered by hop parity.
+    const bool spec = a.spec_next && a.merge_warp && a.early_next && pipe;
+    uint32_t ucur = ctl->u;
     bool pend = false;  // this lane's row of the pre-issued slice
     if (pipe) {
         const uint32_t u = ctl->u;
@@ -216,10 +230,13 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     TR_MARK(2)
     PH_DECL
     PH_MARK(0)  // phase 0: query load + select_start
-    while (ctl->improved && t < a.hop_limit) {
+    while ((spec || ctl->improved) && t < a.hop_limit) {
         ++t;
         HOP_MARK(t, 0)
-        const uint32_t u = ctl->u;
+        const uint32_t u = spec ? ucur : ctl->u;
+        const uint32_t hb = spec ? (t & 1u) : 0u;  // parity set of pos_* / best_*
+        float* pos_d = m.pos_d + (size_t)hb * 2 * a.R;
+        uint32_t* pos_i = m.pos_i + (size_t)hb * 2 * a.R;
         const uint32_t* arow = a.adj + (size_t)u * a.R;
         if (!pipe) {
             // deg and this warp's first adjacency slice load together (no deg -> row
@@ -269,14 +286,18 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             if (a.early_next) track(valid, dist, e);
         }
         if (a.early_next && evaluates && lane == 0) {
-            ctl->best_k[ew] = bk;
-            ctl->best_i[ew] = bi;
-            ctl->best_n[ew] = bn;
+            ctl->best_k[hb * 4 + ew] = bk;
+            ctl->best_i[hb * 4 + ew] = bi;
+            ctl->best_n[hb * 4 + ew] = bn;
         }
         PH_MARK(1)  // adjacency + gather + distances
         HOP_MARK(t, 2)
         __syncthreads();
         HOP_MARK(t, 3)
+        if (spec && !ctl->imp[(t - 1) & 1u]) {  // hop t-1's merge found nothing new: hop t was
+            --t;                       // speculative — the walk ended after hop t-1
+            break;
+        }
         PH_MARK(2)  // barrier: slowest warp's gather
         // The next node is the minimum of R_temp by closer (greedy_search.cpp:63-67).
         // When the hop's smallest distance is held by exactly one candidate, that
@@ -290,13 +311,13 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         if (a.early_next) {
             uint32_t gk = 0xFFFFFFFFu, gid = kInvalid, gn = 0;
             for (uint32_t v = 0; v < nev; ++v) {
-                const uint32_t k2 = ctl->best_k[v];
+                const uint32_t k2 = ctl->best_k[hb * 4 + v];
                 if (k2 < gk) {
                     gk = k2;
-                    gid = ctl->best_i[v];
-                    gn = ctl->best_n[v];
+                    gid = ctl->best_i[hb * 4 + v];
+                    gn = ctl->best_n[hb * 4 + v];
                 } else if (k2 == gk) {
-                    gn += ctl->best_n[v];
+                    gn += ctl->best_n[hb * 4 + v];
                 }
             }
             early = gn == 1u;  // CTA-uniform
@@ -341,6 +362,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
             if (lane == 0) {
                 if (ni != kInvalid) ctl->u = ni;
                 ctl->improved = updated ? 1u : 0u;
+                ctl->imp[t & 1u] = updated ? 1u : 0u;
                 ctl->evals += deg;
             }
             HOP_MARK(t, 5)
@@ -371,7 +393,8 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
         } else {
             PH_MARK(3)
         }
-        __syncthreads();
+        if (spec) ucur = un;  // no end-of-hop barrier (see above)
+        else __syncthreads();
         HOP_MARK(t, 7)
         TR_MARK(3 + t)
         PH_MARK(4)  // barrier

@@ -679,6 +679,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.merge_warp = (uint32_t)env_int("TSDG_GC_MERGE_WARP", 1);
     a.slice = a.merge_warp ? (uint32_t)std::max(1, std::min(32, env_int("TSDG_GC_SLICE", 32))) : 32u;
     a.early_next = (uint32_t)env_int("TSDG_GC_EARLY", 1);
+    a.spec_next = (uint32_t)env_int("TSDG_GC_SPEC", 1);
     a.ld = idx->ld;
     a.R = idx->R;
     a.n = idx->n;
@@ -710,7 +711,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.off_ctl = c.take(sizeof(GcCtl));
     a.off_list = c.take(32 * 8);
     a.off_query = c.take(a.ld * 4);
-    a.off_pos = c.take((size_t)idx->R * 8);
+    a.off_pos = c.take((size_t)idx->R * 16);  // two parity sets of (distance, id)
     a.off_stage = c.take(kGcWarps * warp_stage * 4, 128);
     a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 + 2 * a.t0 * 4 : 0);
     a.off_rowid = c.take(kGcWarps * 32 * 4);
