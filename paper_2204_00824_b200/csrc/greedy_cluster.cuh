@@ -55,6 +55,8 @@ struct GcArgs {
     uint32_t early_next;    // 1: next node from the evaluating warps' minima
     uint32_t adj_prefetch;  // 1: L2-prefetch the adjacency head + deg_cut of every
                             // evaluated node (the next hop's u is one of them)
+    uint32_t share0;        // 1: warp 0 has no slab of its own (uses warp 1's: it
+                            // gathers only in select_start, before warp 1 starts)
     uint32_t spec_next;     // 1: the evaluating warps run hop t+1 while warp 0 merges
                             // hop t (dropped if that merge changed nothing)
     uint32_t npow2;      // pool size for the in-cluster merge
@@ -192,7 +194,7 @@ __device__ __forceinline__ void gc_query(const GcArgs& a, const GcSmem& m, WarpS
     // Pipelined hops (whole rows in one round): each evaluating warp's first slice of
     // the next hop is issued as soon as the next node is known — while warp 0 runs
     // merge_halves — and completed at the top of the next hop.
-    const bool pipe = a.ld <= a.dch && a.slots >= 32;  // TMA or LDGSTS split gathers
+    const bool pipe = a.ld <= a.dch && a.slots >= a.slice;  // TMA or LDGSTS split gathers
     // Evaluating warps: all, or warps 1.. when warp 0 is kept for combine + merge (its
     // merge then overlaps their gathers).  The hop's edges are spread over them in
     // slices of a.slice positions (warp ew takes positions r*nev*SL + ew*SL + [0, SL)
@@ -549,8 +551,9 @@ __global__ void __launch_bounds__(kGcThreads) greedy_cta_kernel(const GcArgs a) 
     const GcSmem m = gc_smem(a, smem_raw);
     WarpStage w;
     w.sq = m.sq;
+    const uint32_t slab = a.share0 ? (warp > 0 ? warp - 1 : 0) : warp;
     w.stage = reinterpret_cast<float*>(smem_raw + a.off_stage) +
-              (size_t)warp * (STAGE == kStageG4 ? a.slots / 4 * a.gpitch : a.slots * (a.dch + 4));
+              (size_t)slab * (STAGE == kStageG4 ? a.slots / 4 * a.gpitch : a.slots * (a.dch + 4));
     w.bar = reinterpret_cast<uint64_t*>(smem_raw + a.off_bar) + warp;
     w.parity = 0;
     w.rowid = STAGE != kStageTma ? reinterpret_cast<uint32_t*>(smem_raw + a.off_rowid) + warp * 32 : nullptr;

@@ -671,7 +671,8 @@ const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
 // the cluster launch is not possible (then the caller merges walks itself).
 // GcArgs + shared-memory carve of the CTA-per-walk kernels.
 size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greedy_params* p,
-                    bool cluster, cudaStream_t st, uint32_t stage_req = kStageG4) {
+                    bool cluster, cudaStream_t st, uint32_t stage_req = kStageG4,
+                    uint32_t compact_slots = 0) {
     a.vec = idx->vec;
     a.adj = idx->adj;
     a.degcut = get_degcut(idx, p->lambda_cut, st);
@@ -693,6 +694,15 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     while (a.npow2 < p->t0 * 32) a.npow2 <<= 1;
     a.dch = staging_dims(idx->ld);
     a.slots = 32;
+    // compact slab (launch_greedy_cta, for grids above one wave): fewer row slots per
+    // warp and warp 0 (the merge warp, which gathers only in select_start) borrowing
+    // warp 1's slab, so that more CTAs fit on an SM
+    a.share0 = 0;
+    if (compact_slots && a.merge_warp) {
+        a.slots = compact_slots;
+        a.slice = std::min(a.slice, compact_slots);
+        a.share0 = 1;
+    }
     // row staging (TSDG_GC_STAGE=g4|tma|ldgsts): tile::gather4 tensor copies by
     // default when the rows fit one staging round (ld <= dch) and the tensor map
     // encodes; else one bulk copy per row
@@ -712,7 +722,7 @@ size_t fill_gc_args(GcArgs& a, tsdg_gpu_index* idx, uint32_t k, const tsdg_greed
     a.off_list = c.take(32 * 8);
     a.off_query = c.take(a.ld * 4);
     a.off_pos = c.take((size_t)idx->R * 16);  // two parity sets of (distance, id)
-    a.off_stage = c.take(kGcWarps * warp_stage * 4, 128);
+    a.off_stage = c.take((kGcWarps - a.share0) * warp_stage * 4, 128);
     a.off_pool = c.take(a.cluster ? a.npow2 * 8 + (kGcThreads + 1) * 4 + 2 * a.t0 * 4 : 0);
     a.off_rowid = c.take(kGcWarps * 32 * 4);
     return round_up(c.total, 128);
@@ -732,15 +742,32 @@ bool launch_greedy_cta(tsdg_gpu_index* idx, const float* d_queries, uint32_t nq,
                        tsdg_query_stats* d_stats, WalkBuffers* wb, cudaStream_t st) {
     GcArgs a{};
     size_t smem = fill_gc_args(a, idx, k, p, wb == nullptr, st);
-    if (a.stage == kStageG4 && !env_is("TSDG_GC_STAGE", "g4")) {
+    int smem_sm = 0, resv = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, idx->device);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, idx->device);
+    const uint64_t walks = (uint64_t)nq * p->t0;
+    // more walks than one wave of CTAs: the compact slab (20 row slots per warp, the
+    // merge warp borrowing a gather warp's slab) when it fits more CTAs per SM.
+    // TSDG_GC_COMPACT=0|1 forces.
+    {
+        const int cenv = env_int("TSDG_GC_COMPACT", -1);
+        const uint64_t per = (uint64_t)smem_sm / (smem + resv);
+        bool want = cenv == 1 || (cenv < 0 && walks > per * (uint64_t)idx->sm_count);
+        if (want && a.merge_warp) {
+            GcArgs b{};
+            const size_t smem_c = fill_gc_args(b, idx, k, p, wb == nullptr, st, kStageG4, 20);
+            if (cenv == 1 || (uint64_t)smem_sm / (smem_c + resv) > per) {
+                a = b;
+                smem = smem_c;
+            }
+        }
+    }
+    if (a.stage == kStageG4 && !env_is("TSDG_GC_STAGE", "g4") && !a.share0) {
         // the gather4 slab is ~3% larger (128-byte aligned 4-slot groups): when that
         // costs a resident CTA per SM and the grid needs it, stage per row instead
         // (C2, t0=10, batch 64: 117 vs 94 us)
         GcArgs b{};
         const size_t smem_t = fill_gc_args(b, idx, k, p, wb == nullptr, st, kStageTma);
-        int smem_sm = 0, resv = 0;
-        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, idx->device);
-        cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, idx->device);
         const uint64_t per_g4 = (uint64_t)smem_sm / (smem + resv), per_t = (uint64_t)smem_sm / (smem_t + resv);
         if (per_g4 < per_t && (uint64_t)nq * p->t0 > per_g4 * (uint64_t)idx->sm_count) {
             a = b;

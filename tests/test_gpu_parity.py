@@ -349,7 +349,8 @@ def test_greedy_kernels_bit_exact(orc, fixtures, index, golden, golden_meta, mon
     ("1", "1", "tma", {"TSDG_GC_SLICE": "16"}), ("1", "1", "tma", {"TSDG_GC_ADJ_PREFETCH": "1"}),
     ("0", "0", "g4", {}), ("1", "0", "g4", {}), ("1", "1", "g4", {}),
     ("1", "1", "g4", {"TSDG_GC_SLICE": "16"}), ("1", "1", "g4", {"TSDG_GC_SPEC": "0"}),
-    ("1", "1", "tma", {"TSDG_GC_SPEC": "0"})])
+    ("1", "1", "tma", {"TSDG_GC_SPEC": "0"}), ("1", "1", "g4", {"TSDG_GC_COMPACT": "1"}),
+    ("1", "1", "tma", {"TSDG_GC_COMPACT": "1"}), ("1", "0", "g4", {"TSDG_GC_COMPACT": "1"})])
 def test_greedy_cluster_kernel_variants_bit_exact(orc, fixtures, index, golden, golden_meta, monkeypatch,
                                                   merge_warp, early, stage, extra):
     """The greedy cluster kernel's internal variants — warp 0 merging while warps 1-3
