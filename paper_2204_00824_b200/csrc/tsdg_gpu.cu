@@ -667,6 +667,14 @@ const void* vectors_tmap(tsdg_gpu_index* idx, uint32_t box, cudaStream_t st) {
     return dev;
 }
 
+// At index creation (no caller stream, no stream capture in progress): the tensor
+// map the gather4 staging of the greedy and deterministic kernels uses, so that a
+// launch never has to allocate or synchronise for it.
+void make_vectors_tmap(tsdg_gpu_index* idx) {
+    const uint32_t dch = staging_dims(idx->ld);
+    if (idx->ld <= dch) vectors_tmap(idx, dch + 4, idx->stream);
+}
+
 // CTA-per-walk / cluster-per-query greedy (greedy_cluster.cuh).  Returns false when
 // the cluster launch is not possible (then the caller merges walks itself).
 // GcArgs + shared-memory carve of the CTA-per-walk kernels.
@@ -1619,6 +1627,7 @@ int tsdg_gpu_index_create(const float* base, uint32_t n, uint32_t d, const uint6
         cuda_check(cudaMemcpy(idx->lam, hlam.data(), na * 2, cudaMemcpyHostToDevice), "cudaMemcpy(lam)");
         cuda_check(cudaMemcpy(idx->deg_full, hdeg.data(), hdeg.size() * 4, cudaMemcpyHostToDevice),
                    "cudaMemcpy(deg)");
+        make_vectors_tmap(idx);
         *out = own.release();
     });
 }
@@ -1713,6 +1722,7 @@ int tsdg_gpu_index_create_from_files(const char* tsdg_path, const char* vectors_
         if (hbad[1] != ~0ull)
             fail(TSDG_EINVAL, "index_create_from_files: edge target out of range at node " +
                                   std::to_string(hbad[1]));
+        make_vectors_tmap(idx);
         *out = own.release();
     });
 }
